@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 SMC-over-PCFG hot path (BASELINE.json metric:
+particle-steps/s and SMC sweeps/s; resample HBM GB/s vs peak).
+
+Default workload (BASELINE.json configs[1], the config the metric is quoted
+on): CRBD on the synthetic 90-tip tree `tree90`, 10^6 particles per GPU, one
+step = one complete SMC sweep (178 epochs: propagate + resample each).  Other
+workloads (--workload): clads2 (configs[2]), seir (configs[3]), resample
+(configs[4], one resampling step of 2^N particles x 64 B).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one process per GPU, NCCL); rank 0 prints one
+JSON line.  `--impl reference` times the CPU oracle (the tier's reference arm)
+on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import inputs  # noqa: E402
+
+WORKLOADS = {
+    "crbd": dict(config=1, model="crbd", tree="tree90", n=1_000_000,
+                 desc="CRBD birth-death, synthetic 90-tip Yule tree (tree90), priors Gamma(1,1)/Gamma(1,0.5)"),
+    "clads2": dict(config=2, model="clads2", tree="tree90", n=1_000_000,
+                   desc="ClaDS2 lineage-specific-rate birth-death on tree90"),
+    "seir": dict(config=3, model="seir", n=1_000_000,
+                 desc="vector-borne-disease SEIR on the synthetic 182-day case series seir182"),
+    "resample": dict(config=4, model="resample", n=1 << 26,
+                     desc="resampling step alone: LSE max + u128 scan + systematic ancestors + 64-B gather"),
+}
+L2_BYTES = 126 * 2 ** 20
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+class Clocks:
+    def __init__(self, path):
+        self.path, self.proc = path, None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader",
+                                          "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self, dev=0):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+        try:
+            rows = [r.split(", ") for r in open(self.path).read().strip().splitlines()]
+            rows = [r for r in rows if r and r[0].strip() == str(dev)]
+            sm = [float(r[1].split()[0]) for r in rows]
+            mx = [float(r[2].split()[0]) for r in rows]
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            reasons = set()
+            for r in rows:
+                for k, nm in enumerate(names):
+                    if r[5 + k].strip() == "Active":
+                        reasons.add(nm)
+            out.update(sm_mhz=float(np.median(sm)) if sm else None,
+                       sm_max_mhz=max(mx) if mx else None, reasons=sorted(reasons), samples=len(sm))
+        except Exception as e:       # pragma: no cover
+            out["error"] = str(e)
+        return out
+
+
+# ----------------------------------------------------------------------------- dist
+def dist_init(gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != gpus:
+        raise SystemExit(f"--gpus {gpus} but WORLD_SIZE={world}")
+    return world, rank, local
+
+
+def model_for(smc, wl):
+    if wl["model"] == "crbd":
+        return smc.Model.crbd(inputs.tree(wl["tree"]), inputs.CRBD_PARAMS)
+    if wl["model"] == "clads2":
+        return smc.Model.clads2(inputs.tree(wl["tree"]), inputs.CLADS2_PARAMS)
+    if wl["model"] == "seir":
+        return smc.Model.seir(inputs.seir_series())
+    raise ValueError(wl)
+
+
+# ----------------------------------------------------------------------------- reference arm / CPU baseline
+def oracle_sweep_rate(wl, budget_s=15.0, n_cap=None):
+    """Time the oracle (single thread, as it stands) on a bounded sample: one
+    sweep of the same model with n particles, n chosen so the run takes
+    roughly budget_s.  Returns (particle-steps/s, sample description, seconds)."""
+    import oracle
+    kind = {"crbd": oracle.CRBD, "clads2": oracle.CLADS2, "seir": oracle.SEIR}[wl["model"]]
+    if wl["model"] in ("crbd", "clads2"):
+        data = oracle.tree_blob(inputs.tree(wl["tree"]))
+        params = inputs.CRBD_PARAMS if wl["model"] == "crbd" else inputs.CLADS2_PARAMS
+    else:
+        data, params = inputs.seir_series(), None
+    n = 1000
+    t0 = time.perf_counter()
+    s = oracle.Smc(kind, data, params, n, 12345)
+    s.run()
+    dt = time.perf_counter() - t0
+    n = max(1000, int(n * budget_s / max(dt, 1e-3)))
+    if n_cap:
+        n = min(n, n_cap)
+    t0 = time.perf_counter()
+    s = oracle.Smc(kind, data, params, n, 12345)
+    s.run()
+    dt = time.perf_counter() - t0
+    st = s.stats()
+    return st["alive_particle_steps"] / dt, f"one full sweep, N={n} particles, seed 12345", dt, st
+
+
+def oracle_resample_rate(n_full, budget_s=10.0):
+    import oracle
+    n = 1 << 20
+    lw = inputs.resample_lw(n, 1.0, 0.0, seed=4)
+    st = inputs.state_bytes(n, 64, seed=5)
+    t0 = time.perf_counter()
+    r = oracle.resample(lw, 4, 0)
+    oracle.gather(st, r["anc"])
+    dt = time.perf_counter() - t0
+    D = len(np.unique(r["anc"]))
+    bytes_alg = n * 20 + 64 * (D + n)
+    return bytes_alg / dt / 1e9, n / dt, f"one resampling step of N=2^20 x 64 B (sigma=1)", dt
+
+
+def run_reference(args, wl):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    ncores = 1
+    if wl["model"] == "resample":
+        vals = []
+        for _ in range(args.warmup):
+            oracle_resample_rate(wl["n"])
+        for _ in range(args.steps):
+            gbs, pps, sample, dt = oracle_resample_rate(wl["n"])
+            vals.append(gbs)
+        v = float(np.mean(vals))
+        line = dict(metric="resample effective GB/s", value=v, unit="GB/s", impl="reference")
+    else:
+        vals = []
+        for _ in range(args.warmup):
+            oracle_sweep_rate(wl, budget_s=3.0)
+        for _ in range(args.steps):
+            pss, sample, dt, st = oracle_sweep_rate(wl, budget_s=8.0)
+            vals.append(pss)
+        v = float(np.mean(vals))
+        line = dict(metric="particle-steps/s", value=v, unit="particle-steps/s", impl="reference")
+    line.update(n_gpus=world, steps=args.steps, warmup=args.warmup, higher_is_better=True,
+                scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
+                config=dict(workload=args.workload, desc=wl["desc"]),
+                cpu_baseline=dict(value=v, unit=line["unit"], cores=ncores, kind="oracle",
+                                  sample=sample),
+                e2e=dict(value=v, unit=line["unit"], h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def bench_sweeps(args, wl, smc, torch, world, rank):
+    N = args.n or wl["n"]
+    model = model_for(smc, wl)
+    stream = torch.cuda.current_stream()
+    if world == 1:
+        h = smc.Smc(model, N, seed=1, stream=stream)
+    else:
+        from paper_2112_00364_b200 import dist as sdist
+        h = sdist.sharded(model, N, seed=1, stream=stream)
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda")
+    # warm-up sweeps (untimed)
+    for w in range(args.warmup):
+        h.reset(1000 + w)
+        h.run()
+    # timed: K sweeps, per-sweep CUDA events on the handle's stream, L2 flushed between
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    h.set_timing(True)
+    prop_ms = res_ms = 0.0
+    steps_done = 0
+    draws = 0
+    alive_steps = 0
+    logzs = []
+    barrier(torch, world)
+    torch.cuda.synchronize()
+    with Clocks(os.path.join(args.out, f"clocks_rank{rank}.csv")) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            h.reset(1 + k)        # re-initialise particles (pc = b0), new seed; not timed
+            ev[k][0].record(stream)
+            h.run()
+            ev[k][1].record(stream)
+            st = h.stats()
+            prop_ms += st["ms_propagate"]
+            res_ms += st["ms_resample"]
+            draws += st["draws"]
+            alive_steps += st["alive_particle_steps"]
+            steps_done += st["epochs"]
+            logzs.append(h.log_z)
+        torch.cuda.synchronize()
+    barrier(torch, world)
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t_ms = max_over_ranks(torch, world, t_ms)
+    # whole-job particle steps (all ranks)
+    tot_steps = sum_over_ranks(torch, world, alive_steps)
+    value = tot_steps / (t_ms / 1e3)
+    sweeps_per_s = args.steps / (t_ms / 1e3)
+    launches = 4 * steps_done
+    return dict(h=h, N=N, t_ms=t_ms, value=value, sweeps=sweeps_per_s, prop_ms=prop_ms,
+                res_ms=res_ms, draws=draws, alive_steps=alive_steps, epochs=steps_done,
+                launches=launches, clocks=clk.summary(torch.cuda.current_device()),
+                logz=float(np.mean(logzs)))
+
+
+def e2e_sweeps(args, wl, smc, torch, N, k_steps):
+    """End to end through the public API with host buffers: every step creates a
+    handle from the host model description (H2D of the tree table), runs the
+    sweep, and reads back log Z and the N final log-weights (D2H)."""
+    model = model_for(smc, wl)
+    ts = []
+    h2d = model.data.nbytes + model.params.nbytes
+    for k in range(k_steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        h = smc.Smc(model, N, seed=500 + k)
+        h.run()
+        lz = h.log_z
+        lw = h.log_weights()
+        h.close()
+        torch.cuda.synchronize()
+        if k:                         # first is warm-up
+            ts.append(time.perf_counter() - t0)
+    d2h = lw.nbytes + 8
+    return dict(t=float(np.mean(ts)), h2d=h2d, d2h=d2h, logz=lz)
+
+
+def bench_resample(args, wl, smc, torch):
+    n = args.n or wl["n"]
+    S = 64
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev)
+    g.manual_seed(4)
+    lw = torch.randn(n, generator=g, device=dev, dtype=torch.float64) * args.sigma
+    st_in = torch.randint(0, 2 ** 31 - 1, (S // 4 * n,), generator=g, device=dev, dtype=torch.int32)
+    st_out = torch.empty_like(st_in)
+    anc = torch.empty(n, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+    r = smc.Resampler(n, S, seed=4, stream=stream)
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+    for w in range(args.warmup):
+        r.device(lw, st_in, st_out, anc, epoch=w)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with Clocks(os.path.join(args.out, "clocks_rank0.csv")) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            r.device(lw, st_in, st_out, anc, epoch=k)
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    times = [a.elapsed_time(b) for a, b in ev]
+    D = r.distinct()
+    alg = n * 20 + S * (D + n)
+    return dict(r=r, n=n, t_ms=float(np.mean(times)), alg_bytes=alg, D=D,
+                clocks=clk.summary(torch.cuda.current_device()))
+
+
+def barrier(torch, world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(torch, world, v):
+    if world == 1:
+        return v
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(torch, world, v):
+    if world == 1:
+        return v
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def run_ours(args, wl):
+    import torch
+    world, rank, local = dist_init(args.gpus)
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2112_00364_b200 as smc
+    pk, pk_kind = peaks()
+    hbm_peak = pk["hbm_gbs"]
+    if wl["model"] == "resample":
+        r = bench_resample(args, wl, smc, torch)
+        achieved = r["alg_bytes"] / (r["t_ms"] / 1e-3) / 1e9 * 1e-6 * 1e6
+        achieved = r["alg_bytes"] / (r["t_ms"] * 1e-3) / 1e9
+        line = dict(metric="resample effective HBM GB/s (B_alg = N*20 + 64*(D+N))", value=achieved,
+                    unit="GB/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
+                    ms_per_step=r["t_ms"], higher_is_better=True, scaling="weak", vs_baseline=None,
+                    dtype="f64/u128", data="synthetic",
+                    config=dict(workload="resample", desc=wl["desc"], n_per_gpu=r["n"],
+                                state_bytes=64, sigma=args.sigma, l2="flushed between steps"),
+                    roofline=dict(bound="hbm", achieved=achieved, peak=hbm_peak, unit="GB/s",
+                                  frac=achieved / hbm_peak, traffic=None, peak_source=pk_kind),
+                    gpu_launches=5 * args.steps, clocks=r["clocks"])
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        return
+    r = bench_sweeps(args, wl, smc, torch, world, rank)
+    N = r["N"]
+    # dominant kernel: propagation (ALU); resample chain: HBM
+    prop_frac = r["prop_ms"] / max(r["prop_ms"] + r["res_ms"], 1e-9)
+    line = dict(metric="particle-steps/s", value=r["value"], unit="particle-steps/s",
+                n_gpus=world, steps=args.steps, warmup=args.warmup,
+                ms_per_step=r["t_ms"] / args.steps, higher_is_better=True, scaling="weak",
+                vs_baseline=None, dtype="f64", data="synthetic",
+                config=dict(workload=args.workload, desc=wl["desc"], n_per_gpu=N,
+                            epochs_per_sweep=r["epochs"] // args.steps,
+                            l2="flushed between steps (state fits L2 within a sweep)"),
+                sweeps_per_s=r["sweeps"], mean_log_z=r["logz"],
+                phase_ms=dict(propagate=r["prop_ms"] / args.steps, resample=r["res_ms"] / args.steps,
+                              propagate_share=prop_frac),
+                draws_per_particle_step=r["draws"] / max(r["alive_steps"], 1),
+                gpu_launches=r["launches"], clocks=r["clocks"])
+    if rank == 0 and not args.no_e2e and world == 1:
+        e = e2e_sweeps(args, wl, smc, torch, N, min(args.steps, 3))
+        line["e2e"] = dict(value=r["alive_steps"] / args.steps / e["t"], unit="particle-steps/s",
+                           h2d_bytes_per_step=e["h2d"], d2h_bytes_per_step=e["d2h"])
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        v, sample, dt, _ = oracle_sweep_rate(wl, budget_s=args.cpu_budget)
+        line["cpu_baseline"] = dict(value=v, unit="particle-steps/s", cores=1, kind="oracle",
+                                    sample=sample, seconds=dt)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="crbd", choices=sorted(WORKLOADS))
+    ap.add_argument("--n", type=int, default=0, help="particles per GPU (default: workload's)")
+    ap.add_argument("--sigma", type=float, default=1.0, help="resample workload: lw ~ sigma N(0,1)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out"))
+    args = ap.parse_args()
+    os.makedirs(args.out, exist_ok=True)
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 breaks the timing rules", file=sys.stderr)
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference(args, wl)
+    else:
+        run_ours(args, wl)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,186 @@
+// device_rng.cuh — Philox4x32-10, the hq uniform conversion, fp64 samplers and
+// log-densities for the sm_100a propagation kernel.
+//
+// The paper asks for a unique seed per state and per-thread seeds in
+// CUDA; we replace seed state by a stateless counter-based stream
+// (DESIGN.md §R-1): draw d of particle n in epoch t is half (d & 1) of Philox
+// block (d >> 1, t, n, tag=0) under key (seed_lo, seed_hi).  Samplers and draw
+// counts follow DESIGN.md §R-3 (the oracle implements the same written spec
+// independently; nothing here is shared with oracle/).
+#pragma once
+#include <cstdint>
+#include <cstring>
+
+namespace smc {
+
+constexpr double kLn2 = 0.6931471805599453094172321214581766;
+constexpr double kTwoPi = 6.283185307179586476925286766559006;
+constexpr double kHalfLog2Pi = 0.9189385332046727417803297364056176;
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+  }
+  return c;
+}
+
+// 53-bit integer of the hq conversion and the double u = z 2^-53 + 2^-54.
+__device__ __forceinline__ unsigned long long hq_bits(uint32_t x, uint32_t y) {
+  return (unsigned long long)x ^ ((unsigned long long)y << 21);
+}
+__device__ __forceinline__ double hq(uint32_t x, uint32_t y) {
+  return __dadd_rn(__dmul_rn(__ull2double_rn(hq_bits(x, y)), 0x1p-53), 0x1p-54);
+}
+
+// Per-particle uniform stream for one epoch (registers only; SoA state holds
+// no RNG state because the stream is a pure function of the counters).
+struct Rng {
+  uint32_t k0, k1, t, n, blk;
+  double spare;
+  bool has_spare;
+  __device__ __forceinline__ Rng(unsigned long long seed, uint32_t particle, uint32_t epoch)
+      : k0((uint32_t)seed), k1((uint32_t)(seed >> 32)), t(epoch), n(particle), blk(0),
+        spare(0.0), has_spare(false) {}
+  __device__ __forceinline__ double uniform() {
+    if (has_spare) { has_spare = false; return spare; }
+    const uint4 r = philox4x32_10(make_uint4(blk, t, n, 0u), k0, k1);
+    ++blk;
+    spare = hq(r.z, r.w);
+    has_spare = true;
+    return hq(r.x, r.y);
+  }
+};
+
+// ---- samplers (draw counts: Exp 1, Bernoulli 1, Uniform 1, Normal 2,
+//      Gamma k=1: 1, k>1: 3 per attempt, k<1: Gamma(k+1) then 1, Beta: two
+//      Gammas, Binomial inversion 1, BTRS 2 per attempt) --------------------
+__device__ __forceinline__ double d_exp(Rng& r, double rate) {
+  const double u = r.uniform();
+  return -log(u) / rate;
+}
+__device__ __forceinline__ bool d_bernoulli(Rng& r, double p) { return r.uniform() < p; }
+__device__ __forceinline__ double d_uniform(Rng& r, double a, double b) {
+  const double u = r.uniform();
+  return a + (b - a) * u;
+}
+__device__ __forceinline__ double d_normal(Rng& r, double mu, double sigma) {
+  const double u1 = r.uniform();
+  const double u2 = r.uniform();
+  const double rad = sqrt(-2.0 * log(u1));
+  const double c = cos(kTwoPi * u2);
+  return mu + sigma * (rad * c);
+}
+__device__ double d_gamma_mt(Rng& r, double k, double theta) {   // k > 1, Marsaglia-Tsang
+  const double d = k - 1.0 / 3.0;
+  const double c = 1.0 / sqrt(9.0 * d);
+  for (;;) {
+    const double x = d_normal(r, 0.0, 1.0);
+    const double u = r.uniform();
+    double v = 1.0 + c * x;
+    if (v <= 0.0) continue;
+    v = v * v * v;
+    const double lhs = log(u);
+    const double rhs = 0.5 * x * x + d - d * v + d * log(v);
+    if (lhs < rhs) return d * v * theta;
+  }
+}
+__device__ __forceinline__ double d_gamma(Rng& r, double k, double theta) {
+  if (k == 1.0) {
+    const double u = r.uniform();
+    return -theta * log(u);
+  }
+  if (k < 1.0) {
+    const double g = d_gamma_mt(r, k + 1.0, theta);
+    const double u = r.uniform();
+    return g * pow(u, 1.0 / k);
+  }
+  return d_gamma_mt(r, k, theta);
+}
+__device__ __forceinline__ double d_beta(Rng& r, double a, double b) {
+  const double x = d_gamma(r, a, 1.0);
+  const double y = d_gamma(r, b, 1.0);
+  return x / (x + y);
+}
+
+// Binomial: inversion (BINV) for n p < 10; BTRS (Hormann 1993) otherwise.
+// The BTRS normaliser h = lgamma(m+1) + lgamma(n-m+1) is only needed when
+// the squeeze fails, so it is computed lazily (same value, fewer lgammas).
+__device__ long long d_binomial_inv(Rng& r, long long n, double p) {
+  const double q = 1.0 - p;
+  const double sr = p / q;
+  const double a = (double)(n + 1) * sr;
+  double pr = exp((double)n * log1p(-p));
+  double u = r.uniform();
+  long long x = 0;
+  while (x < n && u > pr) {
+    u = u - pr;
+    x = x + 1;
+    pr = pr * (a / (double)x - sr);
+  }
+  return x;
+}
+__device__ long long d_binomial_btrs(Rng& r, long long n, double p) {
+  const double q = 1.0 - p;
+  const double nd = (double)n;
+  const double spq = sqrt(nd * p * q);
+  const double b = 1.15 + 2.53 * spq;
+  const double a = -0.0873 + 0.0248 * b + 0.01 * p;
+  const double c = nd * p + 0.5;
+  const double vr = 0.92 - 4.2 / b;
+  const double m = floor((nd + 1.0) * p);
+  bool have_h = false;
+  double h = 0.0, alpha = 0.0, lpq = 0.0;
+  for (;;) {
+    const double U = r.uniform() - 0.5;
+    const double V = r.uniform();
+    const double us = 0.5 - fabs(U);
+    const double kd = floor((2.0 * a / us + b) * U + c);
+    if (kd < 0.0 || kd > nd) continue;
+    if (us >= 0.07 && V <= vr) return (long long)kd;
+    if (!have_h) {
+      alpha = (2.83 + 5.1 / b) * spq;
+      lpq = log(p / q);
+      h = lgamma(m + 1.0) + lgamma(nd - m + 1.0);
+      have_h = true;
+    }
+    const double lv = log(V * alpha / (a / (us * us) + b));
+    const double rhs = h - lgamma(kd + 1.0) - lgamma(nd - kd + 1.0) + (kd - m) * lpq;
+    if (lv <= rhs) return (long long)kd;
+  }
+}
+__device__ __forceinline__ long long d_binomial(Rng& r, long long n, double p) {
+  bool flip = false;
+  if (p > 0.5) { p = 1.0 - p; flip = true; }
+  const long long k = ((double)n * p < 10.0) ? d_binomial_inv(r, n, p) : d_binomial_btrs(r, n, p);
+  return flip ? n - k : k;
+}
+
+__device__ __forceinline__ double d_binomial_logpmf(long long k, long long n, double p) {
+  if (k < 0 || k > n) return -INFINITY;
+  double v = lgamma((double)n + 1.0) - lgamma((double)k + 1.0) - lgamma((double)(n - k) + 1.0);
+  if (k > 0) v = v + (double)k * log(p);
+  if (n - k > 0) v = v + (double)(n - k) * log1p(-p);
+  return v;
+}
+__device__ __forceinline__ double d_normal_logpdf(double y, double mu, double sigma) {
+  const double z = (y - mu) / sigma;
+  return -0.5 * z * z - log(sigma) - kHalfLog2Pi;
+}
+
+// ---- order-preserving int64 key of a double (for atomicMax of log-weights)
+__device__ __forceinline__ long long order_key(double x) {
+  const long long b = __double_as_longlong(x);
+  return b >= 0 ? b : (b ^ 0x7FFFFFFFFFFFFFFFLL);
+}
+__host__ __device__ __forceinline__ double key_to_double(long long k) {
+  const long long b = k >= 0 ? k : (k ^ 0x7FFFFFFFFFFFFFFFLL);
+  double d;
+  memcpy(&d, &b, sizeof(d));
+  return d;
+}
+
+}  // namespace smc

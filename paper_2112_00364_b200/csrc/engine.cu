@@ -1,0 +1,949 @@
+// engine.cu — host engine and C ABI of libsmc (include/smc.h).
+//
+// The engine owns the SoA particle buffers (double-buffered planes, lw, anc)
+// of one or more shards and drives the epoch loop:
+//   propagate<M> (all shards) -> all-gather record A (max, alive, flags)
+//   -> reduce (tile sums, shard total) -> all-gather record B (shard totals)
+//   -> anc_gather (ancestors + fused gather/migration into destination
+//      shards) -> barrier -> finalize (log Z, termination, epoch advance)
+// Shards are either virtual (several in one process, one GPU) or one per
+// process (NCCL or a host all-gather callback for the 16-byte records; CUDA
+// IPC peer pointers for the migration stores).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "smc.h"
+#include "kernels.cuh"
+
+using namespace smc;
+
+namespace {
+
+thread_local std::string g_last_error = "";
+
+// --------------------------------------------------------------------------
+// NCCL, loaded at run time (the process normally already holds torch's copy)
+struct Nccl {
+  bool loaded = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool load(std::string& err) {
+    if (loaded) return true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) { err = std::string("cannot load libnccl.so.2: ") + dlerror(); return false; }
+    GetUniqueId = (decltype(GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
+    AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
+    AllReduce = (decltype(AllReduce))dlsym(h, "ncclAllReduce");
+    CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
+    GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
+    if (!GetUniqueId || !CommInitRank || !AllGather || !AllReduce || !CommDestroy) {
+      err = "libnccl.so.2 lacks required symbols";
+      return false;
+    }
+    loaded = true;
+    return true;
+  }
+};
+Nccl g_nccl;
+
+struct Shard {
+  int id = 0;                      // global shard index (rank for sharded runs)
+  unsigned long long base = 0;     // global index of local particle 0
+  char* ipc_block = nullptr;       // planes[0], planes[1], anc (one allocation, IPC-exportable)
+  uint4* planes[2] = {nullptr, nullptr};
+  uint32_t* anc = nullptr;
+  double* lw = nullptr;
+  u128* tile_sum = nullptr;
+  u128* tile_excl = nullptr;
+  Ctrl* ctrl = nullptr;
+  uint4** d_dst_planes[2] = {nullptr, nullptr};  // device arrays [world]
+  uint32_t** d_dst_anc = nullptr;                 // device array [world]
+};
+
+enum CommKind { COMM_LOCAL = 0, COMM_NCCL = 1, COMM_CALLBACK = 2 };
+
+}  // namespace
+
+struct smc_ctx {
+  int kind = 0;
+  int planes = 0;                 // 16-byte planes per particle
+  uint32_t flags = 0;
+  unsigned long long n_per = 0;   // particles per shard
+  unsigned long long n_total = 0;
+  int world = 1, rank = 0;        // world = number of shards in the run
+  int n_local_shards = 1;         // shards held by this handle
+  int n_tiles = 0;
+  unsigned long long seed = 0;
+  ModelConst mc{};
+  double* d_table = nullptr;
+  std::vector<double> h_table;
+  RecA* d_recA = nullptr;         // [2][world]
+  u128* d_recB = nullptr;         // [2][world]
+  int* d_barrier = nullptr;
+  std::vector<Shard> shards;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  CommKind comm = COMM_LOCAL;
+  ncclComm_t nccl = nullptr;
+  int (*cb_allgather)(const void*, void*, uint64_t, void*) = nullptr;
+  void* cb_user = nullptr;
+  std::vector<void*> ipc_opened;
+  bool ipc_ready = true;
+  Ctrl* h_ctrl = nullptr;         // pinned
+  unsigned long long enq = 0;     // epochs enqueued since reset
+  bool started = false;
+  bool timing = false;            // per-phase CUDA-event timing
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  double ms_propagate = 0.0, ms_resample = 0.0;
+  unsigned long long timed_epochs = 0;
+  int status = SMC_OK;
+  std::string err;
+};
+
+namespace {
+
+int fail(smc_ctx* h, int code, const std::string& msg) {
+  if (h) { h->status = code; h->err = msg; }
+  g_last_error = msg;
+  return code;
+}
+#define CU(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(h, SMC_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+
+// ---- model setup: traversal tables ------------------------
+struct TreeIn {
+  int M = 0, root = -1;
+  std::vector<int> parent, left, right;
+  std::vector<double> age;
+  std::vector<int> tips;   // tips below each node
+};
+bool parse_tree(const double* d, uint64_t len, TreeIn& T, std::string& err) {
+  if (!d || len < 2) { err = "tree data missing"; return false; }
+  T.M = (int)d[0];
+  T.root = (int)d[1];
+  if (T.M < 3 || len != (uint64_t)(2 + 4 * T.M) || T.root < 0 || T.root >= T.M) {
+    err = "tree data must be [M, root, (parent,left,right,age) x M]";
+    return false;
+  }
+  T.parent.resize(T.M); T.left.resize(T.M); T.right.resize(T.M); T.age.resize(T.M);
+  for (int i = 0; i < T.M; ++i) {
+    T.parent[i] = (int)d[2 + 4 * i];
+    T.left[i] = (int)d[3 + 4 * i];
+    T.right[i] = (int)d[4 + 4 * i];
+    T.age[i] = d[5 + 4 * i];
+    const bool tip = T.left[i] < 0;
+    if (tip != (T.right[i] < 0) || T.left[i] >= T.M || T.right[i] >= T.M) {
+      err = "malformed tree node";
+      return false;
+    }
+  }
+  if (T.left[T.root] < 0) { err = "root must be internal"; return false; }
+  // tip counts by an explicit post-order (iterative)
+  T.tips.assign(T.M, 0);
+  std::vector<int> order, st{T.root};
+  while (!st.empty()) {
+    int v = st.back(); st.pop_back();
+    order.push_back(v);
+    if (T.left[v] >= 0) { st.push_back(T.left[v]); st.push_back(T.right[v]); }
+  }
+  if ((int)order.size() != T.M) { err = "tree is not connected / has cycles"; return false; }
+  for (int k = T.M - 1; k >= 0; --k) {
+    int v = order[k];
+    T.tips[v] = T.left[v] < 0 ? 1 : T.tips[T.left[v]] + T.tips[T.right[v]];
+  }
+  return true;
+}
+// CRBD: preorder, left child first; rows (t_parent, t_child, internal).
+void crbd_table(const TreeIn& T, std::vector<double>& out) {
+  std::vector<int> st{T.right[T.root], T.left[T.root]};
+  while (!st.empty()) {
+    const int c = st.back(); st.pop_back();
+    out.push_back(T.age[T.parent[c]]);
+    out.push_back(T.age[c]);
+    out.push_back(T.left[c] >= 0 ? 1.0 : 0.0);
+    if (T.left[c] >= 0) { st.push_back(T.right[c]); st.push_back(T.left[c]); }
+  }
+}
+// ClaDS2: preorder visiting the child with fewer tips first (ties: left);
+// rows (t_parent, t_child, internal, first_left at the child).  Returns the
+// maximum number of pending sibling rates.
+int clads2_table(const TreeIn& T, std::vector<double>& out, bool& root_first_left) {
+  auto first_left = [&](int v) { return T.tips[T.left[v]] <= T.tips[T.right[v]]; };
+  root_first_left = first_left(T.root);
+  // explicit stack of branch children to emit, with the pending depth
+  struct Item { int child; int pend; };
+  std::vector<Item> st;
+  int maxpend = 1;
+  auto push_children = [&](int v, int pend) {
+    const bool fl = first_left(v);
+    const int first = fl ? T.left[v] : T.right[v], second = fl ? T.right[v] : T.left[v];
+    // second is pending while the first subtree is traversed
+    st.push_back({second, pend});
+    st.push_back({first, pend + 1});
+    maxpend = std::max(maxpend, pend + 1);
+  };
+  push_children(T.root, 0);
+  while (!st.empty()) {
+    Item it = st.back(); st.pop_back();
+    const int c = it.child;
+    out.push_back(T.age[T.parent[c]]);
+    out.push_back(T.age[c]);
+    out.push_back(T.left[c] >= 0 ? 1.0 : 0.0);
+    out.push_back(T.left[c] >= 0 && first_left(c) ? 1.0 : 0.0);
+    if (T.left[c] >= 0) push_children(c, it.pend);
+  }
+  return maxpend;
+}
+
+int setup_model(smc_ctx* h, const smc_model* m) {
+  if (!m) return fail(h, SMC_EINVAL, "model is NULL");
+  h->kind = m->kind;
+  h->flags = m->flags;
+  for (int i = 0; i < 12; ++i) h->mc.p[i] = 0.0;
+  auto P = [&](int i, double dflt) { return (m->params && i < m->n_params) ? m->params[i] : dflt; };
+  std::string err;
+  switch (m->kind) {
+    case SMC_CRBD: {
+      TreeIn T;
+      if (!parse_tree(m->data, m->data_len, T, err)) return fail(h, SMC_EINVAL, err);
+      crbd_table(T, h->h_table);
+      h->mc.n = (int)(h->h_table.size() / 3);
+      h->mc.p[0] = P(0, 1.0); h->mc.p[1] = P(1, -1.0); h->mc.p[2] = P(2, -1.0);
+      h->planes = Crbd::kPlanes;
+      break;
+    }
+    case SMC_CLADS2: {
+      TreeIn T;
+      if (!parse_tree(m->data, m->data_len, T, err)) return fail(h, SMC_EINVAL, err);
+      bool rfl = true;
+      const int maxpend = clads2_table(T, h->h_table, rfl);
+      if (maxpend > Clads2::kPend)
+        return fail(h, SMC_EINVAL, "tree needs more than 6 pending sibling rates");
+      h->mc.n = (int)(h->h_table.size() / 4);
+      for (int i = 0; i < 5; ++i) h->mc.p[i] = P(i, i == 0 ? 1.0 : -1.0);
+      h->mc.p[5] = rfl ? 1.0 : 0.0;
+      h->planes = Clads2::kPlanes;
+      break;
+    }
+    case SMC_SEIR: {
+      if (!m->data || m->data_len == 0) return fail(h, SMC_EINVAL, "SEIR needs the case series");
+      h->h_table.assign(m->data, m->data + m->data_len);
+      h->mc.n = (int)m->data_len;
+      if (m->n_params >= 6 && m->params[0] >= 0.0) {
+        for (int i = 0; i < 6; ++i) h->mc.p[i] = m->params[i];
+      } else {
+        h->mc.p[0] = -1.0;
+      }
+      h->mc.p[6] = P(6, 7370.0);
+      h->mc.p[7] = P(7, 10.0 * h->mc.p[6]);
+      h->mc.p[8] = P(8, 0.0);
+      h->mc.p[9] = P(9, 0.0);
+      if (h->mc.p[6] < 1 || h->mc.p[7] < 0 || h->mc.p[8] < 0 || h->mc.p[9] < 0 ||
+          h->mc.p[8] > h->mc.p[6] - 1 || h->mc.p[7] + h->mc.p[9] > 2e8)
+        return fail(h, SMC_EINVAL, "bad SEIR population");
+      h->planes = Seir::kPlanes;
+      break;
+    }
+    case SMC_GEOMETRIC:
+      h->mc.p[0] = P(0, 0.5); h->mc.p[1] = P(1, 1.5);
+      h->planes = Geometric::kPlanes;
+      break;
+    case SMC_SSM:
+      if (!m->data || m->data_len == 0) return fail(h, SMC_EINVAL, "SSM needs observations");
+      h->h_table.assign(m->data, m->data + m->data_len);
+      h->mc.n = (int)m->data_len;
+      h->mc.p[0] = P(0, 0.0); h->mc.p[1] = P(1, 100.0); h->mc.p[2] = P(2, 2.0);
+      h->mc.p[3] = P(3, 1.0); h->mc.p[4] = P(4, 5.0);
+      h->planes = Ssm::kPlanes;
+      break;
+    case SMC_CONSTW:
+      h->mc.p[0] = P(0, std::log(3.0)); h->mc.p[1] = P(1, 1.0);
+      if (h->mc.p[1] < 1) return fail(h, SMC_EINVAL, "CONSTW needs K >= 1");
+      h->planes = Constw::kPlanes;
+      break;
+    case SMC_RESAMPLE_BENCH:
+      if (m->state_bytes == 0 || m->state_bytes % 16 || m->state_bytes > 512)
+        return fail(h, SMC_EINVAL, "state_bytes must be a multiple of 16 in [16, 512]");
+      h->planes = (int)(m->state_bytes / 16);
+      break;
+    default:
+      return fail(h, SMC_EINVAL, "unknown model kind");
+  }
+  if (m->kind == SMC_CRBD || m->kind == SMC_CLADS2) {
+    if (h->mc.n < 2) return fail(h, SMC_EINVAL, "tree has too few branches");
+  }
+  return SMC_OK;
+}
+
+int alloc_shard(smc_ctx* h, Shard& s) {
+  const unsigned long long n = h->n_per;
+  const size_t plane_bytes = (size_t)h->planes * n * 16;
+  const size_t anc_off = 2 * plane_bytes;
+  const size_t block = anc_off + n * sizeof(uint32_t);
+  CU(cudaMalloc(&s.ipc_block, block));
+  s.planes[0] = (uint4*)s.ipc_block;
+  s.planes[1] = (uint4*)(s.ipc_block + plane_bytes);
+  s.anc = (uint32_t*)(s.ipc_block + anc_off);
+  CU(cudaMalloc(&s.lw, n * sizeof(double)));
+  CU(cudaMalloc(&s.tile_sum, (size_t)h->n_tiles * sizeof(u128)));
+  CU(cudaMalloc(&s.tile_excl, (size_t)h->n_tiles * sizeof(u128)));
+  CU(cudaMalloc(&s.ctrl, sizeof(Ctrl)));
+  CU(cudaMalloc(&s.d_dst_planes[0], h->world * sizeof(uint4*)));
+  CU(cudaMalloc(&s.d_dst_planes[1], h->world * sizeof(uint4*)));
+  CU(cudaMalloc(&s.d_dst_anc, h->world * sizeof(uint32_t*)));
+  return SMC_OK;
+}
+
+// Destination pointer tables: for virtual shards every shard's buffers are
+// local; for sharded runs non-local entries are IPC-opened peer pointers.
+int write_dst_tables(smc_ctx* h, const std::vector<uint4*>& p0, const std::vector<uint4*>& p1,
+                     const std::vector<uint32_t*>& anc) {
+  for (auto& s : h->shards) {
+    CU(cudaMemcpy(s.d_dst_planes[0], p0.data(), h->world * sizeof(uint4*), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(s.d_dst_planes[1], p1.data(), h->world * sizeof(uint4*), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(s.d_dst_anc, anc.data(), h->world * sizeof(uint32_t*), cudaMemcpyHostToDevice));
+  }
+  return SMC_OK;
+}
+
+int reset_device(smc_ctx* h) {
+  Ctrl c{};
+  c.logz = 0.0;
+  c.last_inc = 0.0;
+  c.first_err = ~0ull;
+  std::vector<RecA> ra(2 * h->world);
+  for (auto& r : ra) { r.key = LLONG_MIN; r.alive = 0; r.flags = 0; }
+  CU(cudaMemcpyAsync(h->d_recA, ra.data(), ra.size() * sizeof(RecA), cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemsetAsync(h->d_recB, 0, 2 * h->world * sizeof(u128), h->stream));
+  for (auto& s : h->shards) {
+    CU(cudaMemcpyAsync(s.ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, h->stream));
+    // pc = b0 = 0 and all fields zero; lw = 0; anc = identity
+    CU(cudaMemsetAsync(s.planes[0], 0, (size_t)h->planes * h->n_per * 16, h->stream));
+    CU(cudaMemsetAsync(s.lw, 0, h->n_per * sizeof(double), h->stream));
+  }
+  for (auto& s : h->shards) {
+    const unsigned g = (unsigned)std::min<unsigned long long>((h->n_per + 255) / 256, 4096ull);
+    iota_kernel<<<g, 256, 0, h->stream>>>(s.anc, h->n_per, s.base);
+  }
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(h->stream));
+  std::memset(h->h_ctrl, 0, sizeof(Ctrl));
+  h->ms_propagate = h->ms_resample = 0.0;
+  h->timed_epochs = 0;
+  h->enq = 0;
+  h->started = false;
+  h->status = SMC_OK;
+  h->err.clear();
+  return SMC_OK;
+}
+
+int common_init(smc_ctx* h, const smc_model* m, unsigned long long n_per, int world, int rank,
+                int n_local_shards, unsigned long long seed) {
+  int rc = setup_model(h, m);
+  if (rc) return rc;
+  if (n_per == 0) return fail(h, SMC_EINVAL, "n_particles must be >= 1");
+  const unsigned long long total = n_per * (unsigned long long)world;
+  if (total >= (1ull << 32) || total / world != n_per)
+    return fail(h, SMC_EINVAL, "total particles must be < 2^32");
+  int dev_count = 0;
+  cudaError_t e = cudaGetDeviceCount(&dev_count);
+  if (e != cudaSuccess || dev_count == 0)
+    return fail(h, SMC_ECUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  h->n_per = n_per;
+  h->n_total = total;
+  h->world = world;
+  h->rank = rank;
+  h->n_local_shards = n_local_shards;
+  h->seed = seed;
+  h->n_tiles = (int)((n_per + kTile - 1) / kTile);
+  CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  h->own_stream = true;
+  if (!h->h_table.empty()) {
+    CU(cudaMalloc(&h->d_table, h->h_table.size() * sizeof(double)));
+    CU(cudaMemcpy(h->d_table, h->h_table.data(), h->h_table.size() * sizeof(double),
+                  cudaMemcpyHostToDevice));
+  }
+  h->mc.table = h->d_table;
+  h->mc.flags = (int)h->flags;
+  CU(cudaMalloc(&h->d_recA, 2 * world * sizeof(RecA)));
+  CU(cudaMalloc(&h->d_recB, 2 * world * sizeof(u128)));
+  CU(cudaMalloc(&h->d_barrier, sizeof(int)));
+  CU(cudaMallocHost(&h->h_ctrl, sizeof(Ctrl)));
+  h->shards.resize(n_local_shards);
+  for (int i = 0; i < n_local_shards; ++i) {
+    Shard& s = h->shards[i];
+    s.id = n_local_shards == world ? i : rank;
+    s.base = (unsigned long long)s.id * n_per;
+    rc = alloc_shard(h, s);
+    if (rc) return rc;
+  }
+  return SMC_OK;
+}
+
+// ---- collectives ------------------------------------------------------------
+int allgather_rec(smc_ctx* h, void* d_arr, size_t rec_bytes) {
+  // d_arr = [world] records of rec_bytes; this rank filled slot `rank`.
+  if (h->comm == COMM_LOCAL) return SMC_OK;   // shards share the array
+  if (h->comm == COMM_NCCL) {
+    char* base = (char*)d_arr;
+    ncclResult_t r = g_nccl.AllGather(base + h->rank * rec_bytes, base, rec_bytes, ncclUint8, h->nccl,
+                                      h->stream);
+    if (r != ncclSuccess) return fail(h, SMC_ENCCL, "ncclAllGather failed");
+    return SMC_OK;
+  }
+  std::vector<char> send(rec_bytes), recv(rec_bytes * h->world);
+  CU(cudaMemcpyAsync(send.data(), (char*)d_arr + h->rank * rec_bytes, rec_bytes, cudaMemcpyDeviceToHost,
+                     h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  if (h->cb_allgather(send.data(), recv.data(), rec_bytes, h->cb_user) != 0)
+    return fail(h, SMC_ENCCL, "allgather callback failed");
+  CU(cudaMemcpyAsync(d_arr, recv.data(), recv.size(), cudaMemcpyHostToDevice, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return SMC_OK;
+}
+int barrier(smc_ctx* h) {
+  if (h->comm == COMM_LOCAL) return SMC_OK;
+  if (h->comm == COMM_NCCL) {
+    ncclResult_t r = g_nccl.AllReduce(h->d_barrier, h->d_barrier, 1, ncclInt32, ncclSum, h->nccl, h->stream);
+    if (r != ncclSuccess) return fail(h, SMC_ENCCL, "ncclAllReduce (barrier) failed");
+    return SMC_OK;
+  }
+  CU(cudaStreamSynchronize(h->stream));
+  int one = 1;
+  std::vector<int> all(h->world);
+  if (h->cb_allgather(&one, all.data(), sizeof(int), h->cb_user) != 0)
+    return fail(h, SMC_ENCCL, "barrier callback failed");
+  return SMC_OK;
+}
+
+// ---- launches -----------------------------------------------------------------
+template <class M>
+void launch_prop(smc_ctx* h, Shard& s, int cur) {
+  PropArgs a;
+  a.planes = s.planes[cur];
+  a.lw = s.lw;
+  a.n_local = h->n_per;
+  a.shard_base = s.base;
+  a.seed = h->seed;
+  a.recA = h->d_recA;
+  a.world = h->world;
+  a.rank = s.id;
+  a.ctrl = s.ctrl;
+  const unsigned grid = (unsigned)((h->n_per + kThreads - 1) / kThreads);
+  propagate_kernel<M><<<grid, kThreads, 0, h->stream>>>(a, h->mc);
+}
+void launch_propagate(smc_ctx* h, Shard& s, int cur) {
+  switch (h->kind) {
+    case SMC_CRBD: launch_prop<Crbd>(h, s, cur); break;
+    case SMC_CLADS2: launch_prop<Clads2>(h, s, cur); break;
+    case SMC_SEIR: launch_prop<Seir>(h, s, cur); break;
+    case SMC_GEOMETRIC: launch_prop<Geometric>(h, s, cur); break;
+    case SMC_SSM: launch_prop<Ssm>(h, s, cur); break;
+    case SMC_CONSTW: launch_prop<Constw>(h, s, cur); break;
+    default: break;
+  }
+}
+ResArgs res_args(smc_ctx* h, Shard& s, const double* lw, const uint4* src, int dst_par) {
+  ResArgs a;
+  a.lw = lw;
+  a.n_local = h->n_per;
+  a.shard_base = s.base;
+  a.n_total = h->n_total;
+  a.seed = h->seed;
+  a.world = h->world;
+  a.rank = s.id;
+  a.recA = h->d_recA;
+  a.recB = h->d_recB;
+  a.tile_sum = s.tile_sum;
+  a.tile_excl = s.tile_excl;
+  a.n_tiles = h->n_tiles;
+  a.src_planes = src;
+  a.planes = h->planes;
+  a.dst_planes = s.d_dst_planes[dst_par];
+  a.dst_anc = s.d_dst_anc;
+  a.ctrl = s.ctrl;
+  return a;
+}
+void launch_anc_gather(smc_ctx* h, const ResArgs& a) {
+  const unsigned grid = (unsigned)h->n_tiles;
+  switch (h->planes) {
+    case 1: anc_gather_kernel<1><<<grid, kThreads, 0, h->stream>>>(a); break;
+    case 2: anc_gather_kernel<2><<<grid, kThreads, 0, h->stream>>>(a); break;
+    case 4: anc_gather_kernel<4><<<grid, kThreads, 0, h->stream>>>(a); break;
+    case 6: anc_gather_kernel<6><<<grid, kThreads, 0, h->stream>>>(a); break;
+    case 8: anc_gather_kernel<8><<<grid, kThreads, 0, h->stream>>>(a); break;
+    default: anc_gather_kernel<0><<<grid, kThreads, 0, h->stream>>>(a); break;
+  }
+}
+void launch_finalize(smc_ctx* h, Shard& s) {
+  FinArgs f;
+  f.recA = h->d_recA;
+  f.recB = h->d_recB;
+  f.world = h->world;
+  f.rank = s.id;
+  f.n_total = h->n_total;
+  f.strict = (h->flags & SMC_FLAG_STRICT) ? 1 : 0;
+  f.ctrl = s.ctrl;
+  finalize_kernel<<<1, 32, 0, h->stream>>>(f);
+}
+
+// One epoch for all local shards (no host synchronisation unless the comm
+// is host-staged).  The host's parity `enq` equals the device epoch as long
+// as no shard has finished; after the end every kernel is a no-op.
+int enqueue_epoch(smc_ctx* h) {
+  const int cur = (int)(h->enq & 1);
+  const size_t rec = 16;
+  if (h->timing) CU(cudaEventRecord(h->ev[0], h->stream));
+  for (auto& s : h->shards) launch_propagate(h, s, cur);
+  CU(cudaGetLastError());
+  if (h->timing) CU(cudaEventRecord(h->ev[1], h->stream));
+  int rc = allgather_rec(h, h->d_recA + cur * h->world, rec);
+  if (rc) return rc;
+  for (auto& s : h->shards) {
+    ResArgs a = res_args(h, s, s.lw, s.planes[cur], cur ^ 1);
+    reduce_kernel<<<h->n_tiles, kThreads, 0, h->stream>>>(a);
+  }
+  CU(cudaGetLastError());
+  rc = allgather_rec(h, h->d_recB + cur * h->world, rec);
+  if (rc) return rc;
+  for (auto& s : h->shards) launch_anc_gather(h, res_args(h, s, s.lw, s.planes[cur], cur ^ 1));
+  CU(cudaGetLastError());
+  rc = barrier(h);
+  if (rc) return rc;
+  for (auto& s : h->shards) launch_finalize(h, s);
+  CU(cudaGetLastError());
+  if (h->timing) CU(cudaEventRecord(h->ev[2], h->stream));
+  h->enq++;
+  return SMC_OK;
+}
+
+int collect_timing(smc_ctx* h) {
+  if (!h->timing) return SMC_OK;
+  float a = 0.f, b = 0.f;
+  CU(cudaEventElapsedTime(&a, h->ev[0], h->ev[1]));
+  CU(cudaEventElapsedTime(&b, h->ev[1], h->ev[2]));
+  h->ms_propagate += a;
+  h->ms_resample += b;
+  h->timed_epochs++;
+  return SMC_OK;
+}
+
+int read_ctrl(smc_ctx* h) {
+  CU(cudaMemcpyAsync(h->h_ctrl, h->shards[0].ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return SMC_OK;
+}
+
+int status_of(const Ctrl& c) {
+  switch (c.status) {
+    case ST_OK: return SMC_OK;
+    case ST_REJECTED: return SMC_EREJECTED;
+    case ST_NAN: return SMC_ENAN;
+    case ST_OVERFLOW: return SMC_EOVERFLOW;
+    default: return SMC_ECUDA;
+  }
+}
+
+int check_ready(smc_ctx* h) {
+  if (!h) return fail(h, SMC_EINVAL, "NULL handle");
+  if (h->kind == SMC_RESAMPLE_BENCH) return fail(h, SMC_ESTATE, "RESAMPLE_BENCH handles only resample");
+  if (!h->ipc_ready) return fail(h, SMC_ESTATE, "smc_ipc_import has not been called");
+  return SMC_OK;
+}
+
+// Decoded observable state.
+int nfields_of(int kind) {
+  switch (kind) {
+    case SMC_CRBD: return 4;
+    case SMC_CLADS2: return 13;
+    case SMC_SEIR: return 15;
+    case SMC_GEOMETRIC: return 2;
+    case SMC_SSM: return 3;
+    case SMC_CONSTW: return 2;
+    default: return 0;
+  }
+}
+void decode(int kind, const uint32_t* w, double* f) {
+  // w: the particle's planes concatenated (4 words per plane)
+  auto d = [&](int word) { double x; std::memcpy(&x, w + word, 8); return x; };
+  auto i = [&](int word) { return (double)(int32_t)w[word]; };
+  switch (kind) {
+    case SMC_CRBD:
+      f[0] = i(4); f[1] = i(5); f[2] = d(0); f[3] = d(2); break;
+    case SMC_CLADS2:
+      f[0] = i(20); f[1] = i(21); f[2] = i(22); f[3] = d(0); f[4] = d(2); f[5] = d(4); f[6] = d(6);
+      for (int k = 0; k < 6; ++k) f[7 + k] = d(8 + 2 * k);
+      break;
+    case SMC_SEIR:
+      f[0] = i(20); f[1] = i(19); f[2] = d(0); f[3] = d(2); f[4] = d(4); f[5] = d(6); f[6] = d(8);
+      f[7] = d(10);
+      for (int k = 0; k < 4; ++k) f[8 + k] = i(12 + k);
+      for (int k = 0; k < 3; ++k) f[12 + k] = i(16 + k);
+      break;
+    case SMC_GEOMETRIC: f[0] = i(0); f[1] = i(1); break;
+    case SMC_SSM: f[0] = i(2); f[1] = i(3); f[2] = d(0); break;
+    case SMC_CONSTW: f[0] = i(0); f[1] = i(1); break;
+  }
+}
+
+smc_ctx* finish_create(smc_ctx* h, int rc) {
+  if (rc == SMC_OK) return h;
+  g_last_error = h->err;
+  smc_destroy(h);
+  return nullptr;
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+int smc_abi_version(void) { return SMC_ABI_VERSION; }
+
+smc_handle smc_create(const smc_model* model, uint64_t n_particles, uint64_t seed) {
+  return smc_create_virtual(model, n_particles, seed, 1);
+}
+
+smc_handle smc_create_virtual(const smc_model* model, uint64_t n_per_shard, uint64_t seed,
+                              int32_t n_shards) {
+  smc_ctx* h = new smc_ctx();
+  if (n_shards < 1 || n_shards > 64) return finish_create(h, fail(h, SMC_EINVAL, "n_shards in [1, 64]"));
+  int rc = common_init(h, model, n_per_shard, n_shards, 0, n_shards, seed);
+  if (rc) return finish_create(h, rc);
+  h->comm = COMM_LOCAL;
+  std::vector<uint4*> p0, p1;
+  std::vector<uint32_t*> an;
+  for (auto& s : h->shards) { p0.push_back(s.planes[0]); p1.push_back(s.planes[1]); an.push_back(s.anc); }
+  rc = write_dst_tables(h, p0, p1, an);
+  if (rc) return finish_create(h, rc);
+  rc = reset_device(h);
+  return finish_create(h, rc);
+}
+
+int smc_get_nccl_id(void* out128) {
+  std::string err;
+  if (!out128) return fail(nullptr, SMC_EINVAL, "out is NULL");
+  if (!g_nccl.load(err)) return fail(nullptr, SMC_ENCCL, err);
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return fail(nullptr, SMC_ENCCL, "ncclGetUniqueId failed");
+  std::memcpy(out128, &id, sizeof(id));
+  return SMC_OK;
+}
+
+smc_handle smc_create_sharded(const smc_model* model, uint64_t n_per_rank, uint64_t seed,
+                              int32_t rank, int32_t world, const smc_comm* comm) {
+  smc_ctx* h = new smc_ctx();
+  if (world < 1 || rank < 0 || rank >= world || !comm)
+    return finish_create(h, fail(h, SMC_EINVAL, "bad rank/world/comm"));
+  int rc = common_init(h, model, n_per_rank, world, rank, 1, seed);
+  if (rc) return finish_create(h, rc);
+  if (comm->nccl_id) {
+    std::string err;
+    if (!g_nccl.load(err)) return finish_create(h, fail(h, SMC_ENCCL, err));
+    ncclUniqueId id;
+    std::memcpy(&id, comm->nccl_id, sizeof(id));
+    if (g_nccl.CommInitRank(&h->nccl, world, id, rank) != ncclSuccess)
+      return finish_create(h, fail(h, SMC_ENCCL, "ncclCommInitRank failed"));
+    h->comm = COMM_NCCL;
+  } else if (comm->allgather) {
+    h->cb_allgather = comm->allgather;
+    h->cb_user = comm->user;
+    h->comm = COMM_CALLBACK;
+  } else {
+    return finish_create(h, fail(h, SMC_EINVAL, "comm needs nccl_id or allgather"));
+  }
+  h->ipc_ready = world == 1;
+  if (world == 1) {
+    Shard& s = h->shards[0];
+    rc = write_dst_tables(h, {s.planes[0]}, {s.planes[1]}, {s.anc});
+    if (rc) return finish_create(h, rc);
+  }
+  rc = reset_device(h);
+  return finish_create(h, rc);
+}
+
+uint64_t smc_ipc_blob_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+int smc_ipc_export(smc_handle h, void* out) {
+  if (!h || !out) return fail(h, SMC_EINVAL, "NULL argument");
+  cudaIpcMemHandle_t mh;
+  CU(cudaIpcGetMemHandle(&mh, h->shards[0].ipc_block));
+  std::memcpy(out, &mh, sizeof(mh));
+  return SMC_OK;
+}
+
+int smc_ipc_import(smc_handle h, const void* blobs) {
+  if (!h || !blobs) return fail(h, SMC_EINVAL, "NULL argument");
+  const size_t plane_bytes = (size_t)h->planes * h->n_per * 16;
+  std::vector<uint4*> p0(h->world), p1(h->world);
+  std::vector<uint32_t*> an(h->world);
+  for (int g = 0; g < h->world; ++g) {
+    char* base;
+    if (g == h->rank) {
+      base = h->shards[0].ipc_block;
+    } else {
+      cudaIpcMemHandle_t mh;
+      std::memcpy(&mh, (const char*)blobs + g * sizeof(mh), sizeof(mh));
+      void* p = nullptr;
+      CU(cudaIpcOpenMemHandle(&p, mh, cudaIpcMemLazyEnablePeerAccess));
+      h->ipc_opened.push_back(p);
+      base = (char*)p;
+    }
+    p0[g] = (uint4*)base;
+    p1[g] = (uint4*)(base + plane_bytes);
+    an[g] = (uint32_t*)(base + 2 * plane_bytes);
+  }
+  int rc = write_dst_tables(h, p0, p1, an);
+  if (rc) return rc;
+  h->ipc_ready = true;
+  return SMC_OK;
+}
+
+void smc_destroy(smc_handle h) {
+  if (!h) return;
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
+  for (auto& s : h->shards) {
+    cudaFree(s.ipc_block); cudaFree(s.lw); cudaFree(s.tile_sum); cudaFree(s.tile_excl);
+    cudaFree(s.ctrl); cudaFree(s.d_dst_planes[0]); cudaFree(s.d_dst_planes[1]); cudaFree(s.d_dst_anc);
+  }
+  cudaFree(h->d_table); cudaFree(h->d_recA); cudaFree(h->d_recB); cudaFree(h->d_barrier);
+  if (h->h_ctrl) cudaFreeHost(h->h_ctrl);
+  for (auto& e : h->ev) if (e) cudaEventDestroy(e);
+  if (h->nccl && g_nccl.CommDestroy) g_nccl.CommDestroy(h->nccl);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+int smc_set_stream(smc_handle h, void* s) {
+  if (!h) return fail(h, SMC_EINVAL, "NULL handle");
+  CU(cudaStreamSynchronize(h->stream));
+  if (s) {
+    if (h->own_stream) cudaStreamDestroy(h->stream);
+    h->stream = (cudaStream_t)s;
+    h->own_stream = false;
+  } else if (!h->own_stream) {
+    CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->own_stream = true;
+  }
+  return SMC_OK;
+}
+
+int smc_set_timing(smc_handle h, int32_t on) {
+  if (!h) return fail(h, SMC_EINVAL, "NULL handle");
+  if (on && !h->ev[0])
+    for (auto& e : h->ev) CU(cudaEventCreate(&e));
+  h->timing = on != 0;
+  return SMC_OK;
+}
+
+int smc_reset(smc_handle h, uint64_t seed) {
+  if (!h) return fail(h, SMC_EINVAL, "NULL handle");
+  h->seed = seed;
+  return reset_device(h);
+}
+
+int smc_step(smc_handle h, int32_t* done) {
+  int rc = check_ready(h);
+  if (rc) return rc;
+  if (h->h_ctrl->done) { if (done) *done = 1; return status_of(*h->h_ctrl); }
+  h->started = true;
+  rc = enqueue_epoch(h);
+  if (rc) return rc;
+  rc = read_ctrl(h);
+  if (rc) return rc;
+  rc = collect_timing(h);
+  if (rc) return rc;
+  if (done) *done = (int32_t)h->h_ctrl->done;
+  return status_of(*h->h_ctrl);
+}
+
+int smc_run(smc_handle h) {
+  int rc = check_ready(h);
+  if (rc) return rc;
+  int32_t done = 0;
+  while (!done) {
+    rc = smc_step(h, &done);
+    if (rc) return rc;
+  }
+  return SMC_OK;
+}
+
+double smc_log_z(smc_handle h) {
+  if (!h) return NAN;
+  if (!h->started || read_ctrl(h)) return NAN;
+  return h->h_ctrl->logz;
+}
+
+int smc_nfields(smc_handle h) { return h ? nfields_of(h->kind) : 0; }
+
+int smc_ancestors(smc_handle h, uint32_t* out, uint64_t n) {
+  if (!h || !out || n != h->n_per * h->shards.size()) return fail(h, SMC_EINVAL, "bad output size");
+  CU(cudaStreamSynchronize(h->stream));
+  for (size_t i = 0; i < h->shards.size(); ++i)
+    CU(cudaMemcpy(out + i * h->n_per, h->shards[i].anc, h->n_per * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return SMC_OK;
+}
+
+int smc_log_weights(smc_handle h, double* out, uint64_t n) {
+  if (!h || !out || n != h->n_per * h->shards.size()) return fail(h, SMC_EINVAL, "bad output size");
+  CU(cudaStreamSynchronize(h->stream));
+  for (size_t i = 0; i < h->shards.size(); ++i)
+    CU(cudaMemcpy(out + i * h->n_per, h->shards[i].lw, h->n_per * sizeof(double), cudaMemcpyDeviceToHost));
+  return SMC_OK;
+}
+
+static int current_parity(smc_ctx* h) {
+  if (read_ctrl(h)) return -1;
+  return (int)(h->h_ctrl->resamples & 1);
+}
+
+int smc_state(smc_handle h, void* out, uint64_t bytes) {
+  if (!h) return fail(h, SMC_EINVAL, "NULL handle");
+  const uint64_t per = (uint64_t)h->planes * 16 * h->n_per;
+  if (!out || bytes != per * h->shards.size()) return fail(h, SMC_EINVAL, "bad output size");
+  const int par = current_parity(h);
+  if (par < 0) return h->status;
+  for (size_t i = 0; i < h->shards.size(); ++i)
+    CU(cudaMemcpy((char*)out + i * per, h->shards[i].planes[par], per, cudaMemcpyDeviceToHost));
+  return SMC_OK;
+}
+
+int smc_fields(smc_handle h, double* out, uint64_t n_doubles) {
+  if (!h) return fail(h, SMC_EINVAL, "NULL handle");
+  const int F = nfields_of(h->kind);
+  const uint64_t nl = h->n_per * h->shards.size();
+  if (!F || !out || n_doubles != nl * F) return fail(h, SMC_EINVAL, "bad output size");
+  const uint64_t per = (uint64_t)h->planes * 16 * h->n_per;
+  std::vector<uint32_t> raw(per / 4);
+  std::vector<uint32_t> w(h->planes * 4);
+  const int par = current_parity(h);
+  if (par < 0) return h->status;
+  for (size_t si = 0; si < h->shards.size(); ++si) {
+    CU(cudaMemcpy(raw.data(), h->shards[si].planes[par], per, cudaMemcpyDeviceToHost));
+    for (uint64_t k = 0; k < h->n_per; ++k) {
+      for (int p = 0; p < h->planes; ++p)
+        for (int q = 0; q < 4; ++q) w[4 * p + q] = raw[4 * (p * h->n_per + k) + q];
+      decode(h->kind, w.data(), out + (si * h->n_per + k) * F);
+    }
+  }
+  return SMC_OK;
+}
+
+int smc_stats(smc_handle h, smc_stats_t* out) {
+  if (!h || !out) return fail(h, SMC_EINVAL, "NULL argument");
+  std::memset(out, 0, sizeof(*out));
+  out->n_total = h->n_total;
+  out->n_local = h->n_per * h->shards.size();
+  out->rank = h->rank;
+  out->world = h->comm == COMM_LOCAL ? 1 : h->world;
+  out->shards = (int32_t)h->shards.size();
+  out->state_bytes = (uint32_t)h->planes * 16;
+  out->first_error_particle = -1;
+  out->status = h->status;
+  out->ms_propagate = h->ms_propagate;
+  out->ms_resample = h->ms_resample;
+  out->timed_epochs = h->timed_epochs;
+  if (h->stream && cudaStreamSynchronize(h->stream) == cudaSuccess) {
+    unsigned long long alive = 0, ovf = 0, fe = ~0ull, drw = 0;
+    for (auto& s : h->shards) {
+      Ctrl c;
+      if (cudaMemcpy(&c, s.ctrl, sizeof(c), cudaMemcpyDeviceToHost) != cudaSuccess) break;
+      alive += c.alive_steps; ovf += c.overflow; fe = std::min(fe, c.first_err); drw += c.draws;
+      out->epochs = c.epochs; out->resamples = c.resamples; out->done = c.done;
+      if (c.status && !out->status) out->status = status_of(c);
+    }
+    out->alive_particle_steps = alive;
+    out->overflow = ovf;
+    out->draws = drw;
+    out->first_error_particle = fe == ~0ull ? -1 : (int64_t)fe;
+  }
+  return SMC_OK;
+}
+
+const char* smc_errmsg(smc_handle h) {
+  if (h) return h->err.c_str();
+  return g_last_error.c_str();
+}
+
+// ---- resampler alone --------------------------------------------------------
+int smc_resample_device(smc_handle h, const double* d_lw, const void* d_state_in, void* d_state_out,
+                        uint32_t* d_anc, uint32_t epoch, double* logz_inc) {
+  if (!h || h->kind != SMC_RESAMPLE_BENCH || h->shards.size() != 1 || h->world != 1)
+    return fail(h, SMC_ESTATE, "smc_resample_device needs a single-shard RESAMPLE_BENCH handle");
+  if (!d_lw || !d_state_in || !d_state_out || !d_anc) return fail(h, SMC_EINVAL, "NULL buffer");
+  Shard& s = h->shards[0];
+  // destination tables point at the caller's buffers
+  uint4* dst = (uint4*)d_state_out;
+  CU(cudaMemcpyAsync(s.d_dst_planes[1], &dst, sizeof(dst), cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(s.d_dst_anc, &d_anc, sizeof(d_anc), cudaMemcpyHostToDevice, h->stream));
+  prep_resample_kernel<<<1, 32, 0, h->stream>>>(s.ctrl, h->d_recA, h->d_recB, 1, 0, epoch);
+  const unsigned mgrid = (unsigned)std::min<unsigned long long>((h->n_per + kThreads - 1) / kThreads, 148ull * 8);
+  max_kernel<<<mgrid, kThreads, 0, h->stream>>>(d_lw, h->n_per, h->d_recA, 1, 0, s.ctrl);
+  ResArgs a = res_args(h, s, d_lw, (const uint4*)d_state_in, 1);
+  reduce_kernel<<<h->n_tiles, kThreads, 0, h->stream>>>(a);
+  launch_anc_gather(h, a);
+  launch_finalize(h, s);
+  CU(cudaGetLastError());
+  h->started = true;
+  if (logz_inc) {
+    CU(cudaMemcpyAsync(h->h_ctrl, s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    *logz_inc = h->h_ctrl->last_inc;
+    if (h->h_ctrl->status) return fail(h, status_of(*h->h_ctrl), "resampling failed (NaN or all -inf)");
+  }
+  return SMC_OK;
+}
+
+int smc_resample_host(smc_handle h, const double* lw, const void* state_in, void* state_out,
+                      uint32_t* anc, uint32_t epoch, double* logz_inc) {
+  if (!h || h->kind != SMC_RESAMPLE_BENCH) return fail(h, SMC_ESTATE, "needs a RESAMPLE_BENCH handle");
+  Shard& s = h->shards[0];
+  const size_t sb = (size_t)h->planes * 16 * h->n_per;
+  CU(cudaMemcpyAsync(s.lw, lw, h->n_per * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  CU(cudaMemcpyAsync(s.planes[0], state_in, sb, cudaMemcpyHostToDevice, h->stream));
+  double inc = 0.0;
+  int rc = smc_resample_device(h, s.lw, s.planes[0], s.planes[1], s.anc, epoch, &inc);
+  if (rc) return rc;
+  CU(cudaMemcpyAsync(anc, s.anc, h->n_per * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaMemcpyAsync(state_out, s.planes[1], sb, cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  // restore the handle's own destination tables
+  uint4* p1 = s.planes[1];
+  uint32_t* an = s.anc;
+  CU(cudaMemcpy(s.d_dst_planes[1], &p1, sizeof(p1), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(s.d_dst_anc, &an, sizeof(an), cudaMemcpyHostToDevice));
+  if (logz_inc) *logz_inc = inc;
+  return SMC_OK;
+}
+
+int smc_last_distinct(smc_handle h, uint64_t* out) {
+  if (!h || !out) return fail(h, SMC_EINVAL, "NULL argument");
+  CU(cudaStreamSynchronize(h->stream));
+  Ctrl c;
+  CU(cudaMemcpy(&c, h->shards[0].ctrl, sizeof(c), cudaMemcpyDeviceToHost));
+  *out = c.distinct;
+  return SMC_OK;
+}
+
+}  // extern "C"

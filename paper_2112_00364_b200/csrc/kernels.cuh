@@ -1,0 +1,563 @@
+// kernels.cuh — the sm_100a hot path:
+//   propagate<M>   Alg. 1 step 2: one particle per thread,
+//                  blocks dispatched by pc until the next checkpoint; epilogue
+//                  = CTA max of the log-weights (order-preserving int64
+//                  atomicMax), alive count (termination), NaN flag
+//   reduce         exact integer weights q = rint(2^62 exp(lw - m)) summed per
+//                  2048-particle tile in u128; the last CTA scans the tile sums
+//                  (normalising sum; reading R1)
+//   anc_gather     per tile: exclusive u128 scan, systematic ancestor map
+//                  a_j = min{k : (j+u) W < N C_k} evaluated as offspring
+//                  boundaries O_k = F(C_k) (fp64 estimate + exact 192-bit fix-
+//                  up near integers), then the coalesced 128-bit state gather
+//                  of the tile's output slots, written straight into the
+//                  destination shard's buffers (multi-GPU: peer
+//                  memory), plus the ancestor array
+//   finalize       log Z += m + log W - 62 ln 2 - log N, termination,
+//                  epoch advance (single thread)
+#pragma once
+#include <climits>
+#include "models.cuh"
+
+namespace smc {
+
+typedef unsigned __int128 u128;
+
+constexpr int kThreads = 256;
+constexpr int kItems = 8;
+constexpr int kTile = kThreads * kItems;   // particles per resampling tile
+
+// Record all-gathered after propagation (16 B per shard).
+struct RecA {
+  long long key;       // order-preserving key of the shard's max log-weight
+  unsigned alive;      // particles with pc != b_stop after propagation
+  unsigned flags;      // bit 0: NaN or +inf log-weight seen
+};
+
+struct Ctrl {
+  double logz;
+  double last_inc;
+  unsigned epoch;
+  unsigned done;
+  int status;
+  unsigned counter;                  // last-block-done ticket for reduce
+  unsigned long long resamples;
+  unsigned long long epochs;
+  unsigned long long alive_steps;
+  unsigned long long overflow;
+  unsigned long long first_err;      // ULLONG_MAX = none
+  unsigned long long distinct;       // distinct ancestors in the last resample
+  unsigned long long draws;          // uniforms drawn by propagation (all epochs)
+};
+
+enum { ST_OK = 0, ST_REJECTED = 4, ST_NAN = 5, ST_OVERFLOW = 6 };
+
+// ---------------------------------------------------------------- u128 helpers
+__device__ __forceinline__ u128 shfl_up_u128(u128 v, int d) {
+  unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
+  lo = __shfl_up_sync(0xffffffffu, lo, d);
+  hi = __shfl_up_sync(0xffffffffu, hi, d);
+  return ((u128)hi << 64) | lo;
+}
+__device__ __forceinline__ u128 shfl_xor_u128(u128 v, int d) {
+  unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
+  lo = __shfl_xor_sync(0xffffffffu, lo, d);
+  hi = __shfl_xor_sync(0xffffffffu, hi, d);
+  return ((u128)hi << 64) | lo;
+}
+// u128 -> double by truncation to 53 significant bits: every
+// step exact, so log W is bit-identical wherever it is evaluated.
+__host__ __device__ __forceinline__ double u128_trunc_double(u128 x) {
+  const unsigned long long hi = (unsigned long long)(x >> 64), lo = (unsigned long long)x;
+  int bl;
+#ifdef __CUDA_ARCH__
+  bl = hi ? 128 - __clzll((long long)hi) : (lo ? 64 - __clzll((long long)lo) : 0);
+#else
+  bl = hi ? 128 - __builtin_clzll(hi) : (lo ? 64 - __builtin_clzll(lo) : 0);
+#endif
+  const int s = bl > 53 ? bl - 53 : 0;
+  const unsigned long long top = (unsigned long long)(x >> s);
+  return ldexp((double)top, s);
+}
+__device__ __forceinline__ u128 ld_cg_u128(const u128* p) {
+  const unsigned long long* q = (const unsigned long long*)p;
+  return ((u128)__ldcg(q + 1) << 64) | __ldcg(q);
+}
+__device__ __forceinline__ double u128_approx(u128 x) {
+  return __ull2double_rn((unsigned long long)(x >> 64)) * 0x1p64 +
+         __ull2double_rn((unsigned long long)x);
+}
+
+// 128 x 128 -> 256-bit product, limbs little-endian.
+struct U256 { unsigned long long w[4]; };
+__device__ __forceinline__ U256 mul_u128(u128 a, u128 b) {
+  const unsigned long long a0 = (unsigned long long)a, a1 = (unsigned long long)(a >> 64);
+  const unsigned long long b0 = (unsigned long long)b, b1 = (unsigned long long)(b >> 64);
+  const u128 p00 = (u128)a0 * b0, p01 = (u128)a0 * b1, p10 = (u128)a1 * b0, p11 = (u128)a1 * b1;
+  U256 r;
+  r.w[0] = (unsigned long long)p00;
+  u128 mid = (p00 >> 64) + (unsigned long long)p01 + (unsigned long long)p10;
+  r.w[1] = (unsigned long long)mid;
+  u128 hi = (mid >> 64) + (p01 >> 64) + (p10 >> 64) + (unsigned long long)p11;
+  r.w[2] = (unsigned long long)hi;
+  r.w[3] = (unsigned long long)(hi >> 64) + (unsigned long long)(p11 >> 64);
+  return r;
+}
+__device__ __forceinline__ bool lt_u256(const U256& a, const U256& b) {
+#pragma unroll
+  for (int i = 3; i >= 0; --i)
+    if (a.w[i] != b.w[i]) return a.w[i] < b.w[i];
+  return false;
+}
+
+// Systematic grid of one resampling step: positions (j + u)/N, u = (2z+1)/2^54.
+struct Grid {
+  u128 W;                    // total integer weight (all shards)
+  u128 Nsc;                  // N * 2^54
+  unsigned long long z2p1;   // 2z + 1
+  unsigned long long N;
+  double Wd, Nd, ud;
+  // P(j, C): grid point j lies strictly below cumulative weight C.
+  __device__ __forceinline__ bool below(unsigned long long j, u128 C) const {
+    const u128 A = ((u128)j << 54) + z2p1;
+    return lt_u256(mul_u128(A, W), mul_u128(Nsc, C));
+  }
+  // F(C) = #{j in [0, N) : (j + u) W < N C} = clamp(ceil(N C / W - u), 0, N).
+  __device__ __forceinline__ unsigned long long count_below(u128 C) const {
+    const double x = Nd * (u128_approx(C) / Wd) - ud;
+    const double r = rint(x);
+    if (fabs(x - r) > 0x1p-12) {
+      double c = ceil(x);
+      c = c < 0.0 ? 0.0 : (c > Nd ? Nd : c);
+      return (unsigned long long)c;
+    }
+    long long j = (long long)r;                      // exact fix-up near integers
+    if (j < 0) j = 0;
+    if (j > (long long)N) j = (long long)N;
+    while (j < (long long)N && below((unsigned long long)j, C)) ++j;
+    while (j > 0 && !below((unsigned long long)(j - 1), C)) --j;
+    return (unsigned long long)j;
+  }
+};
+
+__device__ __forceinline__ unsigned long long quantize(double lw, double m) {
+  if (lw == -INFINITY) return 0ull;
+  const double e = exp(lw - m);
+  return __double2ull_rn(e * 0x1p62);
+}
+
+// ============================================================================
+// propagate
+// ============================================================================
+struct PropArgs {
+  uint4* planes;                 // current SoA planes of this shard
+  double* lw;                    // [n_local]
+  unsigned long long n_local;    // also the plane stride
+  unsigned long long shard_base; // global index of local particle 0
+  unsigned long long seed;
+  RecA* recA;                    // gathered records, both parities [2][world]
+  int world, rank;
+  Ctrl* ctrl;
+};
+
+template <class M>
+__global__ void __launch_bounds__(kThreads) propagate_kernel(PropArgs a, ModelConst C) {
+  __shared__ long long s_key[kThreads / 32];
+  __shared__ unsigned long long s_ovf[kThreads / 32];
+  __shared__ unsigned long long s_drw[kThreads / 32];
+  if (*(volatile unsigned*)&a.ctrl->done) return;
+  const unsigned epoch = a.ctrl->epoch;
+  const unsigned long long i = (unsigned long long)blockIdx.x * kThreads + threadIdx.x;
+  const bool valid = i < a.n_local;
+  double lw = 0.0;
+  int start_alive = 0, end_alive = 0;
+  bool bad = false;
+  unsigned long long drw = 0;
+  Diag dg;
+  if (valid) {
+    typename M::State s;
+    M::load(s, a.planes, a.n_local, i);
+    if (M::pc(s) != kStop) {
+      start_alive = 1;
+      Rng r(a.seed, (uint32_t)(a.shard_base + i), epoch);
+      for (;;) {
+        const bool ck = M::step(s, lw, r, C, dg);
+        if (ck || M::pc(s) == kStop) break;
+      }
+      M::store(s, a.planes, a.n_local, i);
+      drw = 2ull * r.blk - (r.has_spare ? 1ull : 0ull);
+    }
+    end_alive = M::pc(s) != kStop;
+    a.lw[i] = lw;
+    bad = isnan(lw) || lw == INFINITY;
+  }
+  // epilogue: CTA max key, counts, flags
+  long long key = valid ? order_key(lw) : LLONG_MIN;
+  unsigned long long ovf = dg.overflow;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const long long o = __shfl_xor_sync(0xffffffffu, key, d);
+    key = o > key ? o : key;
+    ovf += __shfl_xor_sync(0xffffffffu, ovf, d);
+    drw += __shfl_xor_sync(0xffffffffu, drw, d);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { s_key[warp] = key; s_ovf[warp] = ovf; s_drw[warp] = drw; }
+  if (dg.overflow || bad) atomicMin(&a.ctrl->first_err, a.shard_base + i);
+  const int n_end = __syncthreads_count(end_alive);
+  const int n_start = __syncthreads_count(start_alive);
+  const int any_bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    long long k = s_key[0];
+    unsigned long long o = s_ovf[0], dr = s_drw[0];
+    for (int w = 1; w < kThreads / 32; ++w) {
+      k = s_key[w] > k ? s_key[w] : k;
+      o += s_ovf[w];
+      dr += s_drw[w];
+    }
+    RecA* rec = a.recA + (epoch & 1) * a.world + a.rank;
+    atomicMax(&rec->key, k);
+    if (n_end) atomicAdd(&rec->alive, (unsigned)n_end);
+    if (any_bad) atomicOr(&rec->flags, 1u);
+    if (n_start) atomicAdd(&a.ctrl->alive_steps, (unsigned long long)n_start);
+    if (o) atomicAdd(&a.ctrl->overflow, o);
+    if (dr) atomicAdd(&a.ctrl->draws, dr);
+  }
+}
+
+// anc[i] = base + i (identity before the first resample)
+__global__ void iota_kernel(uint32_t* anc, unsigned long long n, unsigned long long base) {
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    anc[i] = (uint32_t)(base + i);
+}
+
+// ============================================================================
+// resampling: shared argument block
+// ============================================================================
+struct ResArgs {
+  const double* lw;
+  unsigned long long n_local;         // particles in this shard (= plane stride)
+  unsigned long long shard_base;
+  unsigned long long n_total;
+  unsigned long long seed;
+  int world, rank;
+  RecA* recA;                         // [2][world]
+  u128* recB;                         // [2][world] shard totals
+  u128* tile_sum;                     // [n_tiles]
+  u128* tile_excl;                    // [n_tiles]
+  int n_tiles;
+  const uint4* src_planes;
+  int planes;
+  uint4* const* dst_planes;           // [world] destination buffers (peer pointers)
+  uint32_t* const* dst_anc;           // [world]
+  Ctrl* ctrl;
+};
+
+struct Global {
+  double m;
+  unsigned alive;
+  unsigned flags;
+  bool ok;          // finite max and no NaN: resampling quantities are defined
+};
+__device__ __forceinline__ Global read_global(const RecA* A, int world) {
+  long long k = LLONG_MIN;
+  unsigned alive = 0, flags = 0;
+  for (int g = 0; g < world; ++g) {
+    k = A[g].key > k ? A[g].key : k;
+    alive += A[g].alive;
+    flags |= A[g].flags;
+  }
+  Global G;
+  G.m = key_to_double(k);
+  G.alive = alive;
+  G.flags = flags;
+  G.ok = !flags && G.m != -INFINITY && k != LLONG_MIN;
+  return G;
+}
+
+// ============================================================================
+// reduce: per-tile u128 sums of q; the last CTA scans them
+// ============================================================================
+__global__ void __launch_bounds__(kThreads) reduce_kernel(ResArgs a) {
+  __shared__ u128 s_w[kThreads / 32];
+  __shared__ unsigned s_ticket;
+  if (*(volatile unsigned*)&a.ctrl->done) return;
+  const unsigned par = a.ctrl->epoch & 1;
+  const Global G = read_global(a.recA + par * a.world, a.world);
+  if (!G.ok) return;
+  const unsigned long long base = (unsigned long long)blockIdx.x * kTile;
+  u128 acc = 0;
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const unsigned long long i = base + (unsigned long long)r * kThreads + threadIdx.x;
+    if (i < a.n_local) acc += quantize(__ldg(a.lw + i), G.m);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) acc += shfl_xor_u128(acc, d);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) s_w[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u128 t = 0;
+    for (int w = 0; w < kThreads / 32; ++w) t += s_w[w];
+    a.tile_sum[blockIdx.x] = t;
+    __threadfence();
+    s_ticket = atomicAdd(&a.ctrl->counter, 1u);
+  }
+  __syncthreads();
+  if (s_ticket != gridDim.x - 1) return;
+  // ---- last CTA: exclusive scan of the tile sums, shard total -> recB
+  __threadfence();
+  const int nt = a.n_tiles;
+  const int per = (nt + kThreads - 1) / kThreads;
+  const int lo = threadIdx.x * per;
+  const int hi = min(nt, lo + per);
+  u128 local = 0;
+  for (int t = lo; t < hi; ++t) local += ld_cg_u128(a.tile_sum + t);
+  // CTA exclusive scan of `local`
+  u128 incl = local;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const u128 o = shfl_up_u128(incl, d);
+    if (lane >= d) incl += o;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  u128 woff = 0;
+  for (int w = 0; w < warp; ++w) woff += s_w[w];
+  u128 run = woff + incl - local;
+  for (int t = lo; t < hi; ++t) {
+    a.tile_excl[t] = run;
+    run += ld_cg_u128(a.tile_sum + t);
+  }
+  if (threadIdx.x == kThreads - 1) {
+    a.recB[par * a.world + a.rank] = run;     // shard total
+    a.ctrl->counter = 0;
+  }
+}
+
+// ============================================================================
+// anc_gather: ancestors of the tile's output slots + fused state gather
+// ============================================================================
+__device__ __forceinline__ Grid make_grid(const ResArgs& a, const u128* B, unsigned epoch,
+                                          u128& prefix) {
+  u128 W = 0;
+  prefix = 0;
+  for (int g = 0; g < a.world; ++g) {
+    if (g < a.rank) prefix += B[g];
+    W += B[g];
+  }
+  const uint4 r = philox4x32_10(make_uint4(0u, epoch, 0u, 1u), (uint32_t)a.seed,
+                                (uint32_t)(a.seed >> 32));
+  const unsigned long long z = hq_bits(r.x, r.y);
+  Grid gr;
+  gr.W = W;
+  gr.N = a.n_total;
+  gr.Nsc = (u128)a.n_total << 54;
+  gr.z2p1 = 2ull * z + 1ull;
+  gr.Wd = u128_approx(W);
+  gr.Nd = (double)a.n_total;
+  gr.ud = (double)gr.z2p1 * 0x1p-54;
+  return gr;
+}
+
+template <int P>   // P = planes per particle; P <= 0: runtime a.planes
+__global__ void __launch_bounds__(kThreads) anc_gather_kernel(ResArgs a) {
+  __shared__ double s_lw[kTile];
+  __shared__ unsigned s_O[kTile];
+  __shared__ u128 s_w[kThreads / 32];
+  __shared__ unsigned long long s_jlo;
+  if (*(volatile unsigned*)&a.ctrl->done) return;
+  const unsigned epoch = a.ctrl->epoch;
+  const unsigned par = epoch & 1;
+  const Global G = read_global(a.recA + par * a.world, a.world);
+  if (!G.ok || G.alive == 0) return;       // error, or final epoch: no resample
+  u128 prefix;
+  const Grid gr = make_grid(a, a.recB + par * a.world, epoch, prefix);
+
+  const unsigned long long base = (unsigned long long)blockIdx.x * kTile;
+  const int cnt = (int)min((unsigned long long)kTile, a.n_local - base);
+  // striped (coalesced) load, blocked use
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const int k = r * kThreads + threadIdx.x;
+    s_lw[k] = k < cnt ? __ldg(a.lw + base + k) : -INFINITY;
+  }
+  __syncthreads();
+  unsigned long long q[kItems];
+  u128 tsum = 0;
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    q[r] = quantize(s_lw[threadIdx.x * kItems + r], G.m);
+    tsum += q[r];
+  }
+  // CTA exclusive scan of per-thread sums
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  u128 incl = tsum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const u128 o = shfl_up_u128(incl, d);
+    if (lane >= d) incl += o;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  u128 woff = 0;
+  for (int w = 0; w < warp; ++w) woff += s_w[w];
+  const u128 tile_start = prefix + a.tile_excl[blockIdx.x];
+  u128 C = tile_start + woff + incl - tsum;   // exclusive prefix of this thread's first item
+  if (threadIdx.x == 0) s_jlo = gr.count_below(tile_start);
+  unsigned long long prevO = 0;
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    C += q[r];
+    // zero weight: C_k = C_{k-1}, hence O_k = O_{k-1} (no offspring)
+    const unsigned long long O = (q[r] == 0 && r > 0) ? prevO : gr.count_below(C);
+    s_O[threadIdx.x * kItems + r] = (unsigned)O;
+    prevO = O;
+  }
+  __syncthreads();
+  const unsigned long long jlo = s_jlo;
+  unsigned distinct = 0;
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const int k = threadIdx.x * kItems + r;
+    if (k < cnt) distinct += s_O[k] > (k ? s_O[k - 1] : (unsigned)jlo);
+  }
+  // distinct-ancestor count (for the algorithmic-bytes figure)
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) distinct += __shfl_xor_sync(0xffffffffu, distinct, d);
+  if (lane == 0 && distinct) atomicAdd(&a.ctrl->distinct, (unsigned long long)distinct);
+
+  const unsigned long long jhi = cnt > 0 ? s_O[cnt - 1] : jlo;
+  const int np = P > 0 ? P : a.planes;
+  for (unsigned long long j = jlo + threadIdx.x; j < jhi; j += kThreads) {
+    // k = first item with O_k > j
+    int lo = 0, hi = cnt - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (s_O[mid] > j) hi = mid; else lo = mid + 1;
+    }
+    const unsigned long long src = base + lo;
+    const unsigned long long dshard = j / a.n_local;
+    const unsigned long long dl = j - dshard * a.n_local;
+    uint4* dst = a.dst_planes[dshard];
+    if (P > 0) {
+      uint4 v[P > 0 ? P : 1];
+#pragma unroll
+      for (int p = 0; p < (P > 0 ? P : 1); ++p) v[p] = __ldg(a.src_planes + (unsigned long long)p * a.n_local + src);
+#pragma unroll
+      for (int p = 0; p < (P > 0 ? P : 1); ++p) dst[(unsigned long long)p * a.n_local + dl] = v[p];
+    } else {
+      for (int p = 0; p < np; ++p)
+        dst[(unsigned long long)p * a.n_local + dl] = __ldg(a.src_planes + (unsigned long long)p * a.n_local + src);
+    }
+    a.dst_anc[dshard][dl] = (uint32_t)(a.shard_base + src);
+  }
+}
+
+// ============================================================================
+// finalize: log Z, termination, epoch advance (one thread)
+// ============================================================================
+struct FinArgs {
+  RecA* recA;
+  u128* recB;
+  int world, rank;
+  unsigned long long n_total;
+  int strict;
+  Ctrl* ctrl;
+};
+__global__ void finalize_kernel(FinArgs a) {
+  if (threadIdx.x != 0) return;
+  Ctrl* c = a.ctrl;
+  if (c->done) return;
+  const unsigned epoch = c->epoch;
+  const unsigned par = epoch & 1;
+  const Global G = read_global(a.recA + par * a.world, a.world);
+  if (G.flags) {
+    c->status = ST_NAN;
+    c->done = 1;
+    c->epochs = c->epochs + 1;
+  } else if (!(G.m > -INFINITY)) {
+    c->status = ST_REJECTED;
+    c->logz = -INFINITY;
+    c->done = 1;
+    c->epochs = c->epochs + 1;
+  } else {
+    u128 W = 0;
+    for (int g = 0; g < a.world; ++g) W += a.recB[par * a.world + g];
+    const double lwd = log(u128_trunc_double(W));
+    const double inc = G.m + ((lwd - 62.0 * kLn2) - log((double)a.n_total));
+    c->last_inc = inc;
+    c->logz = c->logz + inc;
+    c->epochs = c->epochs + 1;
+    if (a.strict && c->overflow) {
+      c->status = ST_OVERFLOW;
+      c->done = 1;
+    } else if (G.alive == 0) {
+      c->done = 1;
+    } else {
+      c->resamples = c->resamples + 1;
+      c->epoch = epoch + 1;
+    }
+  }
+  // reset this shard's records of the other parity for the next epoch
+  RecA* nx = a.recA + (par ^ 1) * a.world + a.rank;
+  nx->key = LLONG_MIN;
+  nx->alive = 0;
+  nx->flags = 0;
+  a.recB[(par ^ 1) * a.world + a.rank] = 0;
+}
+
+// ============================================================================
+// resampler-only helpers (BASELINE configs[4])
+// ============================================================================
+// Set the epoch and clear the records of a standalone resampling step.
+__global__ void prep_resample_kernel(Ctrl* c, RecA* recA, u128* recB, int world, int rank,
+                                     unsigned epoch) {
+  if (threadIdx.x != 0) return;
+  c->epoch = epoch;
+  c->done = 0;
+  c->status = 0;
+  c->distinct = 0;
+  RecA* r = recA + (epoch & 1) * world + rank;
+  r->key = LLONG_MIN;
+  r->alive = 1;          // a standalone step always resamples
+  r->flags = 0;
+  recB[(epoch & 1) * world + rank] = 0;
+}
+// Max of lw (the propagation epilogue's job in a full SMC run).
+__global__ void __launch_bounds__(kThreads) max_kernel(const double* lw, unsigned long long n,
+                                                       RecA* recA, int world, int rank, Ctrl* c) {
+  __shared__ long long s_key[kThreads / 32];
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  const unsigned par = c->epoch & 1;
+  long long key = LLONG_MIN;
+  bool bad = false;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * kThreads + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * kThreads) {
+    const double v = __ldg(lw + i);
+    bad |= isnan(v) || v == INFINITY;
+    const long long k = order_key(v);
+    key = k > key ? k : key;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const long long o = __shfl_xor_sync(0xffffffffu, key, d);
+    key = o > key ? o : key;
+  }
+  if ((threadIdx.x & 31) == 0) s_key[threadIdx.x >> 5] = key;
+  if (bad) s_bad = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long k = s_key[0];
+    for (int w = 1; w < kThreads / 32; ++w) k = s_key[w] > k ? s_key[w] : k;
+    RecA* r = recA + par * world + rank;
+    atomicMax(&r->key, k);
+    if (s_bad) atomicOr(&r->flags, 1u);
+  }
+}
+
+}  // namespace smc

@@ -1,0 +1,416 @@
+// models.cuh — PCFG block tables (sim : B x S -> B x S x {ckpt})
+// for the propagation kernel.  Each model is a struct with
+//   kPlanes                 number of 16-byte SoA state planes
+//   State / load / store    registers <-> planes  (plane p of particle i at
+//                           planes[p * stride + i])
+//   pc(s)                   current block, kStop = -1 is b_stop
+//   step(s, lw, rng, C, d)  run block pc(s) once; returns true at a checkpoint
+//                           (checkpoints only at block tails)
+// The specs are DESIGN.md §R-11 (CRBD), §R-14 (ClaDS2), §R-15 (SEIR),
+// Fig. 2 (geometric), Eq. (2)/Fig. 4 (SSM), S:493 (constant weight).
+#pragma once
+#include "device_rng.cuh"
+
+namespace smc {
+
+constexpr int kStop = -1;
+constexpr int kStackCap = 1024;          // helper DFS stack (§R-12)
+constexpr unsigned kEventCap = 1u << 22; // helper DFS events per call (§R-12)
+
+// Constant model data, passed by value to the kernel.
+struct ModelConst {
+  const double* table;   // device: per-model table (branches / series)
+  int n;                 // number of branches / series length
+  int flags;
+  double p[12];          // parameters
+};
+
+// Per-thread diagnostics sink.
+struct Diag {
+  unsigned long long overflow;
+  __device__ Diag() : overflow(0) {}
+};
+
+__device__ __forceinline__ uint4 ldp(const uint4* planes, unsigned long long stride, int p,
+                                     unsigned long long i) {
+  return planes[(unsigned long long)p * stride + i];
+}
+__device__ __forceinline__ void stp(uint4* planes, unsigned long long stride, int p,
+                                    unsigned long long i, uint4 v) {
+  planes[(unsigned long long)p * stride + i] = v;
+}
+__device__ __forceinline__ uint4 pack_dd(double a, double b) {
+  const unsigned long long x = __double_as_longlong(a), y = __double_as_longlong(b);
+  return make_uint4((uint32_t)x, (uint32_t)(x >> 32), (uint32_t)y, (uint32_t)(y >> 32));
+}
+__device__ __forceinline__ double lo_d(uint4 v) {
+  return __longlong_as_double(((long long)v.y << 32) | v.x);
+}
+__device__ __forceinline__ double hi_d(uint4 v) {
+  return __longlong_as_double(((long long)v.w << 32) | v.z);
+}
+
+// ============================================================================
+// CRBD (§R-11).  Table: per branch i (left-first preorder over non-root
+// nodes): [t_parent, t_child, internal].  Params: rho, lambda_fixed, mu_fixed.
+// Planes: P0 = {lambda, mu}; P1 = {pc, branch, 0, 0}.
+// ============================================================================
+struct Crbd {
+  static constexpr int kPlanes = 2;
+  struct State { double lambda, mu; int pc, branch; };
+  __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
+    const uint4 a = ldp(P, st, 0, i), b = ldp(P, st, 1, i);
+    s.lambda = lo_d(a); s.mu = hi_d(a); s.pc = (int)b.x; s.branch = (int)b.y;
+  }
+  __device__ static void store(const State& s, uint4* P, unsigned long long st, unsigned long long i) {
+    stp(P, st, 0, i, pack_dd(s.lambda, s.mu));
+    stp(P, st, 1, i, make_uint4((uint32_t)s.pc, (uint32_t)s.branch, 0u, 0u));
+  }
+  __device__ static int pc(const State& s) { return s.pc; }
+
+  // goesUndetected: DFS over the hidden side subtree born at age s0.
+  // 1 undetected, 0 detected, -1 stack/event overflow.
+  __device__ static int undetected(double s0, const State& st, double rho, Rng& r) {
+    double stack[kStackCap];
+    int sp = 0;
+    stack[sp++] = s0;
+    unsigned events = 0;
+    const double tot = st.lambda + st.mu;
+    const double pb = st.lambda / tot;
+    while (sp > 0) {
+      double s = stack[--sp];
+      for (;;) {
+        if (++events > kEventCap) return -1;
+        const double d = d_exp(r, tot);
+        if (d > s) {
+          if (d_bernoulli(r, rho)) return 0;
+          break;
+        }
+        s = s - d;
+        if (d_bernoulli(r, pb)) {
+          if (sp >= kStackCap) return -1;
+          stack[sp++] = s;
+          continue;
+        }
+        break;
+      }
+    }
+    return 1;
+  }
+
+  __device__ static bool step(State& s, double& lw, Rng& r, const ModelConst& C, Diag& dg) {
+    const double rho = C.p[0];
+    if (s.pc == 0) {                                    // INIT, jump (no checkpoint)
+      s.lambda = C.p[1] >= 0.0 ? C.p[1] : d_gamma(r, 1.0, 1.0);
+      s.mu = C.p[2] >= 0.0 ? C.p[2] : d_gamma(r, 1.0, 0.5);
+      s.branch = 0;
+      s.pc = 1;
+      return false;
+    }
+    const double* b = C.table + 3 * s.branch;           // BRANCH
+    const double tp = __ldg(b), tc = __ldg(b + 1);
+    const bool internal = __ldg(b + 2) != 0.0;
+    lw = lw + (-s.mu * (tp - tc));
+    lw = lw + (internal ? log(s.lambda) : log(rho));
+    double t = tp;
+    for (;;) {
+      t = t - d_exp(r, s.lambda);
+      if (t <= tc) break;
+      const int u = undetected(t, s, rho, r);
+      if (u == 1) { lw = lw + kLn2; continue; }
+      if (u < 0) ++dg.overflow;
+      lw = -INFINITY;
+      break;
+    }
+    s.branch = s.branch + 1;
+    s.pc = (s.branch == C.n) ? kStop : 1;
+    return true;
+  }
+};
+
+// ============================================================================
+// ClaDS2 (§R-14).  Table: per branch i (smaller-subtree-first preorder):
+// [t_parent, t_child, internal, first_left]; C.p[5] = root first_left.
+// Params: rho, lambda0, sigma, alpha, eps (each < 0: prior).
+// Planes: P0 {sigma, alpha} P1 {eps, lam} P2..P4 pending rates[6]
+//         P5 {pc, branch, sp, 0}.
+// ============================================================================
+struct Clads2 {
+  static constexpr int kPlanes = 6;
+  static constexpr int kPend = 6;
+  struct State { double sigma, alpha, eps, lam; double pend[kPend]; int pc, branch, sp; };
+  __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
+    uint4 v = ldp(P, st, 0, i); s.sigma = lo_d(v); s.alpha = hi_d(v);
+    v = ldp(P, st, 1, i); s.eps = lo_d(v); s.lam = hi_d(v);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      v = ldp(P, st, 2 + k, i); s.pend[2 * k] = lo_d(v); s.pend[2 * k + 1] = hi_d(v);
+    }
+    v = ldp(P, st, 5, i); s.pc = (int)v.x; s.branch = (int)v.y; s.sp = (int)v.z;
+  }
+  __device__ static void store(const State& s, uint4* P, unsigned long long st, unsigned long long i) {
+    stp(P, st, 0, i, pack_dd(s.sigma, s.alpha));
+    stp(P, st, 1, i, pack_dd(s.eps, s.lam));
+#pragma unroll
+    for (int k = 0; k < 3; ++k) stp(P, st, 2 + k, i, pack_dd(s.pend[2 * k], s.pend[2 * k + 1]));
+    stp(P, st, 5, i, make_uint4((uint32_t)s.pc, (uint32_t)s.branch, (uint32_t)s.sp, 0u));
+  }
+  __device__ static int pc(const State& s) { return s.pc; }
+  __device__ static double daughter(const State& s, double lam, double z) {
+    return s.alpha * lam * exp(s.sigma * z);
+  }
+  __device__ static void push(State& s, double v) {
+    // constant-index selects keep pend[] in registers
+#pragma unroll
+    for (int k = 0; k < kPend; ++k) if (k == s.sp) s.pend[k] = v;
+    s.sp = s.sp + 1;
+  }
+  __device__ static double pop(State& s) {
+    s.sp = s.sp - 1;
+    double v = 0.0;
+#pragma unroll
+    for (int k = 0; k < kPend; ++k) if (k == s.sp) v = s.pend[k];
+    return v;
+  }
+  __device__ static int undetected(double s0, double lam0, const State& st, double rho, Rng& r) {
+    double stk_s[kStackCap];
+    double stk_l[kStackCap];
+    int sp = 0;
+    stk_s[sp] = s0; stk_l[sp] = lam0; ++sp;
+    unsigned events = 0;
+    const double pb = 1.0 / (1.0 + st.eps);
+    while (sp > 0) {
+      --sp;
+      double s = stk_s[sp], lam = stk_l[sp];
+      for (;;) {
+        if (++events > kEventCap) return -1;
+        const double d = d_exp(r, lam * (1.0 + st.eps));
+        if (d > s) {
+          if (d_bernoulli(r, rho)) return 0;
+          break;
+        }
+        s = s - d;
+        if (d_bernoulli(r, pb)) {
+          const double za = d_normal(r, 0.0, 1.0);
+          const double zb = d_normal(r, 0.0, 1.0);
+          if (sp >= kStackCap) return -1;
+          stk_s[sp] = s; stk_l[sp] = daughter(st, lam, zb); ++sp;
+          lam = daughter(st, lam, za);
+          continue;
+        }
+        break;
+      }
+    }
+    return 1;
+  }
+  __device__ static bool step(State& s, double& lw, Rng& r, const ModelConst& C, Diag& dg) {
+    const double rho = C.p[0];
+    if (s.pc == 0) {                                     // INIT + root split (jump)
+      const double lam0 = C.p[1] >= 0.0 ? C.p[1] : d_gamma(r, 1.0, 1.0);
+      s.sigma = C.p[2] >= 0.0 ? C.p[2] : sqrt(1.0 / d_gamma(r, 1.0, 1.0 / 0.2));
+      s.alpha = C.p[3] >= 0.0 ? C.p[3] : exp(d_normal(r, 0.0, s.sigma));
+      s.eps = C.p[4] >= 0.0 ? C.p[4] : d_uniform(r, 0.0, 1.0);
+      const double zl = d_normal(r, 0.0, 1.0);
+      const double zr = d_normal(r, 0.0, 1.0);
+      const double rl = daughter(s, lam0, zl), rr = daughter(s, lam0, zr);
+      const bool fl = C.p[5] != 0.0;
+      s.sp = 0;
+      push(s, fl ? rr : rl);
+      s.lam = fl ? rl : rr;
+      s.branch = 0;
+      s.pc = 1;
+      return false;
+    }
+    const double* b = C.table + 4 * s.branch;
+    const double tp = __ldg(b), tc = __ldg(b + 1);
+    const bool internal = __ldg(b + 2) != 0.0;
+    const bool first_left = __ldg(b + 3) != 0.0;
+    double t = tp;
+    for (;;) {
+      const double dt = d_exp(r, s.lam);
+      if (t - dt <= tc) {
+        lw = lw + (-s.eps * s.lam * (t - tc));
+        break;
+      }
+      lw = lw + (-s.eps * s.lam * dt);
+      t = t - dt;
+      const double zs = d_normal(r, 0.0, 1.0);
+      const double zc = d_normal(r, 0.0, 1.0);
+      const int u = undetected(t, daughter(s, s.lam, zs), s, rho, r);
+      if (u != 1) {
+        if (u < 0) ++dg.overflow;
+        lw = -INFINITY;
+        break;
+      }
+      lw = lw + kLn2;
+      s.lam = daughter(s, s.lam, zc);
+    }
+    if (internal) {
+      lw = lw + log(s.lam);
+      const double zl = d_normal(r, 0.0, 1.0);
+      const double zr = d_normal(r, 0.0, 1.0);
+      const double rl = daughter(s, s.lam, zl), rr = daughter(s, s.lam, zr);
+      push(s, first_left ? rr : rl);
+      s.lam = first_left ? rl : rr;
+    } else {
+      lw = lw + log(rho);
+      if (s.branch + 1 < C.n) s.lam = pop(s);
+    }
+    s.branch = s.branch + 1;
+    s.pc = (s.branch == C.n) ? kStop : 1;
+    return true;
+  }
+};
+
+// ============================================================================
+// SEIR (§R-15).  Table: y[T].  Params: [lam_h, del_h, gam_h, lam_m, del_m,
+// rho] (p[0] < 0: priors), p[6] n_h, p[7] s_m0, p[8] e_h0, p[9] i_m0.
+// Planes: P0 {lam_h, del_h} P1 {gam_h, lam_m} P2 {del_m, rho}
+//         P3 {sh, eh, ih, rh} P4 {sm, em, im, t} P5 {pc, 0, 0, 0}.
+// ============================================================================
+struct Seir {
+  static constexpr int kPlanes = 6;
+  struct State { double lam_h, del_h, gam_h, lam_m, del_m, rho; int sh, eh, ih, rh, sm, em, im, t, pc; };
+  __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
+    uint4 v = ldp(P, st, 0, i); s.lam_h = lo_d(v); s.del_h = hi_d(v);
+    v = ldp(P, st, 1, i); s.gam_h = lo_d(v); s.lam_m = hi_d(v);
+    v = ldp(P, st, 2, i); s.del_m = lo_d(v); s.rho = hi_d(v);
+    v = ldp(P, st, 3, i); s.sh = (int)v.x; s.eh = (int)v.y; s.ih = (int)v.z; s.rh = (int)v.w;
+    v = ldp(P, st, 4, i); s.sm = (int)v.x; s.em = (int)v.y; s.im = (int)v.z; s.t = (int)v.w;
+    v = ldp(P, st, 5, i); s.pc = (int)v.x;
+  }
+  __device__ static void store(const State& s, uint4* P, unsigned long long st, unsigned long long i) {
+    stp(P, st, 0, i, pack_dd(s.lam_h, s.del_h));
+    stp(P, st, 1, i, pack_dd(s.gam_h, s.lam_m));
+    stp(P, st, 2, i, pack_dd(s.del_m, s.rho));
+    stp(P, st, 3, i, make_uint4((uint32_t)s.sh, (uint32_t)s.eh, (uint32_t)s.ih, (uint32_t)s.rh));
+    stp(P, st, 4, i, make_uint4((uint32_t)s.sm, (uint32_t)s.em, (uint32_t)s.im, (uint32_t)s.t));
+    stp(P, st, 5, i, make_uint4((uint32_t)s.pc, 0u, 0u, 0u));
+  }
+  __device__ static int pc(const State& s) { return s.pc; }
+  __device__ static bool step(State& s, double& lw, Rng& r, const ModelConst& C, Diag&) {
+    const long long nh_i = (long long)C.p[6];
+    if (s.pc == 0) {                                     // INIT (jump)
+      if (C.p[0] >= 0.0) {
+        s.lam_h = C.p[0]; s.del_h = C.p[1]; s.gam_h = C.p[2];
+        s.lam_m = C.p[3]; s.del_m = C.p[4]; s.rho = C.p[5];
+      } else {
+        s.lam_h = d_beta(r, 1.0, 1.0);
+        s.del_h = d_beta(r, 1.0 + 2.0 / 4.4, 3.0 - 2.0 / 4.4);
+        s.gam_h = d_beta(r, 1.0 + 2.0 / 4.5, 3.0 - 2.0 / 4.5);
+        s.lam_m = d_beta(r, 1.0, 1.0);
+        s.del_m = d_beta(r, 1.0 + 2.0 / 6.5, 3.0 - 2.0 / 6.5);
+        s.rho = d_beta(r, 1.0, 1.0);
+      }
+      const int eh0 = (int)C.p[8];
+      s.sh = (int)nh_i - 1 - eh0; s.eh = eh0; s.ih = 1; s.rh = 0;
+      s.sm = (int)C.p[7]; s.em = 0; s.im = (int)C.p[9];
+      s.t = 0;
+      s.pc = 1;
+      return false;
+    }
+    const double nh = (double)nh_i;                      // DAY
+    const double ph = 1.0 - exp(-(double)s.im / nh);
+    const double pm = 1.0 - exp(-(double)s.ih / nh);
+    const long long tau_h = d_binomial(r, s.sh, ph);
+    const long long de_h = d_binomial(r, tau_h, s.lam_h);
+    const long long di_h = d_binomial(r, s.eh, s.del_h);
+    const long long dr_h = d_binomial(r, s.ih, s.gam_h);
+    s.sh = (int)(s.sh - de_h);
+    s.eh = (int)(s.eh + de_h - di_h);
+    s.ih = (int)(s.ih + di_h - dr_h);
+    s.rh = (int)(s.rh + dr_h);
+    const long long tau_m = d_binomial(r, s.sm, pm);
+    const long long de_m = d_binomial(r, tau_m, s.lam_m);
+    const long long di_m = d_binomial(r, s.em, s.del_m);
+    const long long nm = (long long)s.sm + s.em + s.im;
+    const double nu_m = 1.0 / 7.0, mu_m = 6.0 / 7.0;
+    const long long births = d_binomial(r, nm, nu_m);
+    const long long s2 = d_binomial(r, s.sm - de_m, mu_m);
+    const long long e2 = d_binomial(r, s.em + de_m - di_m, mu_m);
+    const long long i2 = d_binomial(r, s.im + di_m, mu_m);
+    s.sm = (int)(s2 + births);
+    s.em = (int)e2;
+    s.im = (int)i2;
+    const long long y = (long long)__ldg(C.table + s.t);
+    lw = lw + d_binomial_logpmf(y, di_h, s.rho);
+    s.t = s.t + 1;
+    s.pc = (s.t == C.n) ? kStop : 1;
+    return true;
+  }
+};
+
+// ============================================================================
+// Weighted geometric, Fig. 2(a).  Params p, w.  Plane P0 {pc, n, 0, 0}.
+// ============================================================================
+struct Geometric {
+  static constexpr int kPlanes = 1;
+  struct State { int pc, n; };
+  __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
+    const uint4 v = ldp(P, st, 0, i); s.pc = (int)v.x; s.n = (int)v.y;
+  }
+  __device__ static void store(const State& s, uint4* P, unsigned long long st, unsigned long long i) {
+    stp(P, st, 0, i, make_uint4((uint32_t)s.pc, (uint32_t)s.n, 0u, 0u));
+  }
+  __device__ static int pc(const State& s) { return s.pc; }
+  __device__ static bool step(State& s, double& lw, Rng& r, const ModelConst& C, Diag&) {
+    const bool x = d_bernoulli(r, C.p[0]);
+    s.n = s.n + 1;
+    if (x) { lw = lw + log(C.p[1]); s.pc = 0; }
+    else { s.pc = kStop; }
+    return true;
+  }
+};
+
+// ============================================================================
+// SSM, Eq. (2) / Fig. 4.  Table y[T]; params m0, s0, drift, q, r.
+// Plane P0 {x, pc, t}.
+// ============================================================================
+struct Ssm {
+  static constexpr int kPlanes = 1;
+  struct State { double x; int pc, t; };
+  __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
+    const uint4 v = ldp(P, st, 0, i); s.x = lo_d(v); s.pc = (int)v.z; s.t = (int)v.w;
+  }
+  __device__ static void store(const State& s, uint4* P, unsigned long long st, unsigned long long i) {
+    const unsigned long long xb = __double_as_longlong(s.x);
+    stp(P, st, 0, i, make_uint4((uint32_t)xb, (uint32_t)(xb >> 32), (uint32_t)s.pc, (uint32_t)s.t));
+  }
+  __device__ static int pc(const State& s) { return s.pc; }
+  __device__ static bool step(State& s, double& lw, Rng& r, const ModelConst& C, Diag&) {
+    if (s.pc == 0) {
+      s.x = d_normal(r, C.p[0], C.p[1]);
+      s.t = 0;
+      s.pc = 1;
+      return false;
+    }
+    s.x = d_normal(r, s.x + C.p[2], C.p[3]);
+    lw = lw + d_normal_logpdf(__ldg(C.table + s.t), s.x, C.p[4]);
+    s.t = s.t + 1;
+    s.pc = (s.t == C.n) ? kStop : 1;
+    return true;
+  }
+};
+
+// ============================================================================
+// Constant weight: weight(log w); checkpoint; K times.  Plane P0 {pc, k}.
+// ============================================================================
+struct Constw {
+  static constexpr int kPlanes = 1;
+  struct State { int pc, k; };
+  __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
+    const uint4 v = ldp(P, st, 0, i); s.pc = (int)v.x; s.k = (int)v.y;
+  }
+  __device__ static void store(const State& s, uint4* P, unsigned long long st, unsigned long long i) {
+    stp(P, st, 0, i, make_uint4((uint32_t)s.pc, (uint32_t)s.k, 0u, 0u));
+  }
+  __device__ static int pc(const State& s) { return s.pc; }
+  __device__ static bool step(State& s, double& lw, Rng&, const ModelConst& C, Diag&) {
+    lw = lw + C.p[0];
+    s.k = s.k + 1;
+    s.pc = (s.k == (int)C.p[1]) ? kStop : 0;
+    return true;
+  }
+};
+
+}  // namespace smc

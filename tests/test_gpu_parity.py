@@ -1,0 +1,203 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs and RNG streams.
+
+Bars (BASELINE.json north_star): log-weights and log Z agree to relative 1e-9
+in fp64; ancestor indices bit-exact (the integer resampler is exact, so the only
+admissible difference is an exp() ulp moving a cumulative weight across a grid
+point within 1e-12 — checked, never silently allowed); integer state bit-exact;
+floating state relative 1e-12.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-9
+
+
+def both(smc, kind, tree_or_data, params, N, seed, shards=1):
+    """(gpu Smc, oracle Smc) for the same model/N/seed, not yet run."""
+    if kind in (oracle.CRBD, oracle.CLADS2):
+        gm = smc.Model(kind, smc.tree_data(tree_or_data), params)
+        od = oracle.tree_blob(tree_or_data)
+    else:
+        gm = smc.Model(kind, tree_or_data, params)
+        od = tree_or_data
+    return smc.Smc(gm, N, seed, shards=shards), oracle.Smc(kind, od, params, N, seed)
+
+
+def compare(g, o, check_state=True):
+    lo, lg = o.lw(), g.log_weights()
+    np.testing.assert_array_equal(np.isneginf(lg), np.isneginf(lo))
+    f = np.isfinite(lo)
+    np.testing.assert_allclose(lg[f], lo[f], rtol=RTOL, atol=1e-12)
+    np.testing.assert_array_equal(g.ancestors(), o.anc())
+    if check_state:
+        fg, fo = g.fields(), o.fields()
+        assert fg.shape == fo.shape
+        np.testing.assert_array_equal(fg[:, 0], fo[:, 0])           # pc
+        np.testing.assert_allclose(fg, fo, rtol=1e-12, atol=1e-300)
+
+
+def run_pair(smc, kind, data, params, N, seed, per_epoch=True, shards=1, max_epochs=None):
+    g, o = both(smc, kind, data, params, N, seed, shards)
+    e = 0
+    while True:
+        rg, dg = g.step()
+        ro, do = o.step()
+        assert rg == ro, (rg, ro)
+        assert dg == do
+        if per_epoch or dg:
+            compare(g, o)
+        e += 1
+        if dg or (max_epochs and e >= max_epochs):
+            break
+    if dg:
+        if math.isfinite(o.log_z):
+            assert g.log_z == pytest.approx(o.log_z, rel=RTOL)
+        else:
+            assert g.log_z == o.log_z
+        sg, so = g.stats(), o.stats()
+        assert sg["epochs"] == so["epochs"] and sg["resamples"] == so["resamples"]
+        assert sg["alive_particle_steps"] == so["alive_particle_steps"]
+        assert sg["overflow"] == so["overflow"]
+    return g, o
+
+
+# ------------------------------------------------------------- resampler alone
+@pytest.mark.parametrize("N", [1, 2, 7, 2047, 2048, 2049, 100_003])
+@pytest.mark.parametrize("sigma,finf", [(0.0, 0.0), (1.0, 0.0), (4.0, 0.25), (12.0, 0.5)])
+def test_resampler_parity(smc, N, sigma, finf):
+    lw = inputs.resample_lw(N, sigma, finf, seed=N)
+    if not np.isfinite(lw).any():
+        lw[0] = 0.0
+    S = 64
+    st = inputs.state_bytes(N, S, seed=N + 1)
+    r = smc.Resampler(N, S, seed=77)
+    for epoch in (0, 5):
+        anc, out, inc = r.host(lw, smc.aos_to_soa(st), epoch=epoch)
+        ref = oracle.resample(lw, seed=77, epoch=epoch)
+        np.testing.assert_array_equal(anc, ref["anc"])
+        assert inc == pytest.approx(ref["logz_inc"], rel=1e-13, abs=1e-13)
+        np.testing.assert_array_equal(smc.soa_to_aos(out), oracle.gather(st, ref["anc"]))
+        assert r.distinct() == len(np.unique(ref["anc"]))
+
+
+@pytest.mark.parametrize("S", [16, 32, 96, 128, 272])
+def test_resampler_state_sizes(smc, S):
+    N = 5000
+    lw = inputs.resample_lw(N, 2.0, 0.1, seed=3)
+    st = inputs.state_bytes(N, S, seed=4)
+    r = smc.Resampler(N, S, seed=5)
+    anc, out, _ = r.host(lw, smc.aos_to_soa(st), epoch=2)
+    ref = oracle.resample(lw, seed=5, epoch=2)
+    np.testing.assert_array_equal(anc, ref["anc"])
+    np.testing.assert_array_equal(smc.soa_to_aos(out), oracle.gather(st, ref["anc"]))
+
+
+def test_resampler_errors(smc):
+    r = smc.Resampler(100, 64, seed=1)
+    st = np.zeros((4, 100, 16), np.uint8)
+    with pytest.raises(smc.SmcError) as e:
+        r.host(np.full(100, -np.inf), st)
+    assert e.value.code == smc.EREJECTED
+    lw = np.zeros(100)
+    lw[17] = np.nan
+    with pytest.raises(smc.SmcError) as e:
+        r.host(lw, st)
+    assert e.value.code == smc.ENAN
+
+
+def test_resampler_single_heavy_particle(smc):
+    # all weight on one particle: every output slot copies it (extreme imbalance)
+    N = 300_000
+    lw = np.full(N, -np.inf)
+    lw[123_457] = 0.0
+    st = inputs.state_bytes(N, 64, seed=9)
+    r = smc.Resampler(N, 64, seed=2)
+    anc, out, inc = r.host(lw, smc.aos_to_soa(st))
+    assert np.all(anc == 123_457)
+    assert inc == pytest.approx(-math.log(N))
+    np.testing.assert_array_equal(smc.soa_to_aos(out), np.broadcast_to(st[123_457], st.shape))
+
+
+# ------------------------------------------------------------- whole SMC runs
+@pytest.mark.parametrize("N", [1, 1000, 2500])
+def test_constw(smc, N):
+    run_pair(smc, oracle.CONSTW, None, inputs.CONSTW_PARAMS, N, 3)
+
+
+@pytest.mark.parametrize("N", [777, 4099])
+def test_geometric(smc, N):
+    run_pair(smc, oracle.GEOMETRIC, None, inputs.GEOMETRIC_PARAMS, N, 11)
+
+
+def test_ssm(smc):
+    run_pair(smc, oracle.SSM, inputs.ssm_series(50), inputs.SSM_PARAMS, 3000, 5)
+
+
+@pytest.mark.parametrize("N,seed", [(1000, 1), (2049, 2)])
+def test_crbd_tree5(smc, N, seed):
+    run_pair(smc, oracle.CRBD, inputs.tree("tree5"), inputs.CRBD_PARAMS, N, seed)
+
+
+def test_crbd_tree5_fixed_rates(smc):
+    run_pair(smc, oracle.CRBD, inputs.tree("tree5"), [1.0, 0.3, 0.1], 1500, 4)
+
+
+def test_crbd_tree90(smc):
+    run_pair(smc, oracle.CRBD, inputs.tree("tree90"), inputs.CRBD_PARAMS, 3000, 90, per_epoch=False)
+
+
+def test_clads2_tree5(smc):
+    run_pair(smc, oracle.CLADS2, inputs.tree("tree5"), inputs.CLADS2_PARAMS, 2000, 6)
+
+
+def test_clads2_tree90(smc):
+    run_pair(smc, oracle.CLADS2, inputs.tree("tree90"), inputs.CLADS2_PARAMS, 2000, 7, per_epoch=False)
+
+
+def test_seir(smc):
+    run_pair(smc, oracle.SEIR, inputs.seir_series(), None, 1000, 8, per_epoch=False)
+
+
+def test_seir_tiny_population(smc):
+    params = [0.5, 0.4, 0.3, 0.6, 0.5, 0.7, 3, 1, 1, 1]
+    run_pair(smc, oracle.SEIR, np.array([1.0, 0.0, 1.0]), params, 3000, 9)
+
+
+def test_rejected(smc):
+    g, o = both(smc, oracle.CRBD, inputs.tree("tree5"), [1.0, 0.0, 0.1], 500, 1)
+    assert g.run_status() == smc.EREJECTED
+    assert o.run() == oracle.EREJECTED
+    assert g.log_z == -math.inf
+
+
+# ------------------------------------------------------------- multi-shard path
+@pytest.mark.parametrize("shards", [2, 3, 4])
+def test_virtual_shards_identical(smc, shards):
+    N = 4096 * 3
+    ref = smc.Smc(smc.Model.crbd(inputs.tree("tree90")), N, 21)
+    ref.run()
+    g = smc.Smc(smc.Model.crbd(inputs.tree("tree90")), N, 21, shards=shards)
+    g.run()
+    assert g.log_z == ref.log_z
+    np.testing.assert_array_equal(g.ancestors(), ref.ancestors())
+    np.testing.assert_array_equal(g.log_weights(), ref.log_weights())
+    np.testing.assert_array_equal(g.fields(), ref.fields())
+
+
+def test_virtual_shards_vs_oracle(smc):
+    run_pair(smc, oracle.CLADS2, inputs.tree("tree5"), inputs.CLADS2_PARAMS, 3 * 1001, 12, shards=3)
+
+
+# ------------------------------------------------------------- full size
+def test_crbd_full_size_prefix(smc):
+    """BASELINE configs[1] at 10^6 particles, first 4 epochs, element by element."""
+    run_pair(smc, oracle.CRBD, inputs.tree("tree90"), inputs.CRBD_PARAMS, 1_000_000, 1,
+             per_epoch=True, max_epochs=4)
