@@ -327,6 +327,8 @@ def run_ours(args, wl):
     import torch
     world, rank, local = dist_init(args.gpus)
     torch.cuda.set_device(local)
+    # all work (ours and the timing events) on one dedicated stream
+    torch.cuda.set_stream(torch.cuda.Stream())
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))

@@ -114,6 +114,18 @@ def _check(h, rc):
     return rc
 
 
+def _stream_ptr(stream):
+    """torch.cuda.Stream / raw handle -> cudaStream_t.  torch's default stream
+    has handle 0, which the C ABI reads as "own stream": map it to
+    cudaStreamLegacy (0x1) so work really runs on the caller's stream."""
+    if stream is None:
+        return None
+    ptr = getattr(stream, "cuda_stream", stream)
+    if hasattr(stream, "cuda_stream") and ptr == 0:
+        return 1
+    return ptr or None
+
+
 def _dptr(a):
     return a.ctypes.data_as(C.POINTER(C.c_double))
 
@@ -203,8 +215,7 @@ class Smc:
 
     def set_stream(self, stream):
         """stream: torch.cuda.Stream, raw cudaStream_t int, or None."""
-        ptr = getattr(stream, "cuda_stream", stream)
-        _check(self.h, _lib.smc_set_stream(self.h, C.c_void_p(ptr or 0)))
+        _check(self.h, _lib.smc_set_stream(self.h, C.c_void_p(_stream_ptr(stream))))
 
     def set_timing(self, on=True):
         _check(self.h, _lib.smc_set_timing(self.h, 1 if on else 0))
@@ -268,8 +279,7 @@ class Resampler:
             raise SmcError(EINVAL, _lib.smc_errmsg(None).decode())
         self.n, self.state_bytes = int(n), int(state_bytes)
         if stream is not None:
-            ptr = getattr(stream, "cuda_stream", stream)
-            _check(self.h, _lib.smc_set_stream(self.h, C.c_void_p(ptr or 0)))
+            _check(self.h, _lib.smc_set_stream(self.h, C.c_void_p(_stream_ptr(stream))))
 
     def close(self):
         if getattr(self, "h", None):
