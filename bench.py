@@ -201,15 +201,14 @@ def bench_sweeps(args, wl, smc, torch, world, rank):
         from paper_2112_00364_b200 import dist as sdist
         h = sdist.sharded(model, N, seed=1, stream=stream)
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda")
-    # warm-up sweeps (untimed)
+    # warm-up sweeps (untimed; the first also captures the whole-run CUDA graph)
     for w in range(args.warmup):
         h.reset(1000 + w)
         h.run()
-    # timed: K sweeps, per-sweep CUDA events on the handle's stream, L2 flushed between
+    # timed: K sweeps (one graph launch each), per-sweep CUDA events on the
+    # handle's stream, L2 flushed between sweeps (outside the events)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    h.set_timing(True)
-    prop_ms = res_ms = 0.0
     steps_done = 0
     draws = 0
     alive_steps = 0
@@ -224,8 +223,6 @@ def bench_sweeps(args, wl, smc, torch, world, rank):
             h.run()
             ev[k][1].record(stream)
             st = h.stats()
-            prop_ms += st["ms_propagate"]
-            res_ms += st["ms_resample"]
             draws += st["draws"]
             alive_steps += st["alive_particle_steps"]
             steps_done += st["epochs"]
@@ -238,7 +235,20 @@ def bench_sweeps(args, wl, smc, torch, world, rank):
     tot_steps = sum_over_ranks(torch, world, alive_steps)
     value = tot_steps / (t_ms / 1e3)
     sweeps_per_s = args.steps / (t_ms / 1e3)
-    launches = 4 * steps_done
+    # phase split, measured live with CUDA events around each epoch's kernels
+    # (host-stepped sweeps with the same seeds; not part of the headline time)
+    h.set_timing(True)
+    prop_ms = res_ms = 0.0
+    for k in range(args.steps):
+        h.reset(1 + k)
+        h.run()
+        st = h.stats()
+        prop_ms += st["ms_propagate"]
+        res_ms += st["ms_resample"]
+    h.set_timing(False)
+    # graph body = 2 epochs x (propagate, reduce, anc_gather, finalize) + set_condition
+    E = steps_done // args.steps
+    launches = args.steps * 9 * ((E + 1) // 2)
     return dict(h=h, N=N, t_ms=t_ms, value=value, sweeps=sweeps_per_s, prop_ms=prop_ms,
                 res_ms=res_ms, draws=draws, alive_steps=alive_steps, epochs=steps_done,
                 launches=launches, clocks=clk.summary(torch.cuda.current_device()),

@@ -164,6 +164,12 @@ int smc_set_stream(smc_handle h, void* cuda_stream);
 
 /* --- running ---------------------------------------------------------------- */
 
+/* smc_run as ONE CUDA graph launch (default on): a WHILE conditional node
+ * repeats {epoch, epoch} until the device sets done; no host round trip per
+ * epoch.  Off: a host loop of smc_step (needed with a host all-gather comm or
+ * per-phase timing, which force the host loop automatically). */
+int smc_set_graph(smc_handle h, int32_t on);
+
 /* Per-phase CUDA-event timing of every epoch (off by default).  The times
  * accumulate into smc_stats_t.ms_propagate / ms_resample until smc_reset. */
 int smc_set_timing(smc_handle h, int32_t on);

@@ -341,6 +341,10 @@ struct CrbdModel {
 };
 
 // ---- ClaDS2 (BASELINE.json configs[2]; not in PAPER.md) -----
+// Rate guard: a lineage rate above kMaxRate (or not finite)
+// is outside the model's support; the particle's weight becomes -inf and the
+// block ends at once ("kill": branch index and pc advance, nothing else).
+const double CLADS2_MAX_RATE = 1e4;
 struct Clads2Model {
   std::vector<Branch> br;
   double rho = 1.0, lam0_fixed = -1.0, sigma_fixed = -1.0, alpha_fixed = -1.0, eps_fixed = -1.0;
@@ -358,9 +362,11 @@ struct Clads2Model {
     f[5] = s.eps; f[6] = s.lam;
     for (int i = 0; i < PEND; ++i) f[7 + i] = s.pend[i];
   }
+  static bool bad_rate(double r) { return !(r <= CLADS2_MAX_RATE); }
   double daughter(const State& s, double lam, double z) const {
     return s.alpha * lam * std::exp(s.sigma * z);
   }
+  // 1 undetected, 0 detected or rate out of range, -1 stack/event overflow
   int undetected(double s0, double lam0, const State& st, Stream& rs) const {
     std::vector<std::pair<double, double>> stack;
     stack.push_back(std::make_pair(s0, lam0));
@@ -380,14 +386,22 @@ struct Clads2Model {
         if (sample_bernoulli(rs, pb)) {
           double za = sample_normal(rs, 0.0, 1.0);
           double zb = sample_normal(rs, 0.0, 1.0);
+          double la = daughter(st, lam, za), lb = daughter(st, lam, zb);
+          if (bad_rate(la) || bad_rate(lb)) return 0;
           if (stack.size() >= stack_cap) return -1;
-          stack.push_back(std::make_pair(s, daughter(st, lam, zb)));
-          lam = daughter(st, lam, za);
+          stack.push_back(std::make_pair(s, lb));
+          lam = la;
           continue;
         }
         break;
       }
     }
+    return 1;
+  }
+  int kill(State& s, double& lw) const {
+    lw = -INFINITY;
+    s.branch = s.branch + 1;
+    s.pc = (s.branch == (int)br.size()) ? PC_STOP : 1;
     return 1;
   }
   int step(State& s, double& lw, Stream& rs, uint64_t& overflow) const {
@@ -409,6 +423,7 @@ struct Clads2Model {
       return 0;
     }
     const Branch& b = br[s.branch];
+    if (bad_rate(s.lam)) return kill(s, lw);
     double t = b.tp;
     for (;;) {
       double dt = sample_exp(rs, s.lam);
@@ -420,20 +435,23 @@ struct Clads2Model {
       t = t - dt;
       double zs = sample_normal(rs, 0.0, 1.0);
       double zc = sample_normal(rs, 0.0, 1.0);
-      int r = undetected(t, daughter(s, s.lam, zs), s, rs);
+      double ls = daughter(s, s.lam, zs);
+      if (bad_rate(ls)) return kill(s, lw);
+      int r = undetected(t, ls, s, rs);
       if (r != 1) {
         if (r < 0) ++overflow;
-        lw = -INFINITY;
-        break;
+        return kill(s, lw);
       }
       lw = lw + LN2;
       s.lam = daughter(s, s.lam, zc);
+      if (bad_rate(s.lam)) return kill(s, lw);
     }
     if (b.internal) {
       lw = lw + std::log(s.lam);
       double zl = sample_normal(rs, 0.0, 1.0);
       double zr = sample_normal(rs, 0.0, 1.0);
       double rl = daughter(s, s.lam, zl), rr = daughter(s, s.lam, zr);
+      if (bad_rate(rl) || bad_rate(rr)) return kill(s, lw);
       s.pend[s.sp++] = b.first_left ? rr : rl;
       s.lam = b.first_left ? rl : rr;
     } else {

@@ -78,6 +78,7 @@ _sig = {
     "smc_set_stream": ([H, C.c_void_p], C.c_int),
     "smc_reset": ([H, C.c_uint64], C.c_int),
     "smc_set_timing": ([H, C.c_int32], C.c_int),
+    "smc_set_graph": ([H, C.c_int32], C.c_int),
     "smc_run": ([H], C.c_int),
     "smc_step": ([H, C.POINTER(C.c_int32)], C.c_int),
     "smc_log_z": ([H], C.c_double),
@@ -216,6 +217,9 @@ class Smc:
     def set_stream(self, stream):
         """stream: torch.cuda.Stream, raw cudaStream_t int, or None."""
         _check(self.h, _lib.smc_set_stream(self.h, C.c_void_p(_stream_ptr(stream))))
+
+    def set_graph(self, on=True):
+        _check(self.h, _lib.smc_set_graph(self.h, 1 if on else 0))
 
     def set_timing(self, on=True):
         _check(self.h, _lib.smc_set_timing(self.h, 1 if on else 0))

@@ -110,6 +110,10 @@ struct smc_ctx {
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   double ms_propagate = 0.0, ms_resample = 0.0;
   unsigned long long timed_epochs = 0;
+  bool use_graph = true;          // whole run as one graph launch (WHILE conditional node)
+  cudaGraphExec_t graph_exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaStream_t cap_stream = nullptr;
   int status = SMC_OK;
   std::string err;
 };
@@ -329,6 +333,7 @@ int reset_device(smc_ctx* h) {
   c.logz = 0.0;
   c.last_inc = 0.0;
   c.first_err = ~0ull;
+  c.seed = h->seed;
   std::vector<RecA> ra(2 * h->world);
   for (auto& r : ra) { r.key = LLONG_MIN; r.alive = 0; r.flags = 0; }
   CU(cudaMemcpyAsync(h->d_recA, ra.data(), ra.size() * sizeof(RecA), cudaMemcpyHostToDevice, h->stream));
@@ -442,7 +447,6 @@ void launch_prop(smc_ctx* h, Shard& s, int cur) {
   a.lw = s.lw;
   a.n_local = h->n_per;
   a.shard_base = s.base;
-  a.seed = h->seed;
   a.recA = h->d_recA;
   a.world = h->world;
   a.rank = s.id;
@@ -467,7 +471,6 @@ ResArgs res_args(smc_ctx* h, Shard& s, const double* lw, const uint4* src, int d
   a.n_local = h->n_per;
   a.shard_base = s.base;
   a.n_total = h->n_total;
-  a.seed = h->seed;
   a.world = h->world;
   a.rank = s.id;
   a.recA = h->d_recA;
@@ -543,6 +546,43 @@ int collect_timing(smc_ctx* h) {
   h->ms_propagate += a;
   h->ms_resample += b;
   h->timed_epochs++;
+  return SMC_OK;
+}
+
+// One CUDA graph for a whole sweep: WHILE(!done) { epoch (parity 0); epoch
+// (parity 1); set condition }.  Kernel arguments are fixed at capture (buffer
+// pointers, parity); epoch, seed and all per-run state live in device memory.
+int build_graph(smc_ctx* h) {
+  if (h->graph_exec) return SMC_OK;
+  if (!h->cap_stream) CU(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+  CU(cudaGraphCreate(&h->graph, 0));
+  cudaGraphConditionalHandle hdl;
+  CU(cudaGraphConditionalHandleCreate(&hdl, h->graph, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams np{};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = hdl;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  CU(cudaGraphAddNode(&node, h->graph, nullptr, 0, &np));
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  cudaStream_t keep = h->stream;
+  const unsigned long long keep_enq = h->enq;
+  h->stream = h->cap_stream;
+  CU(cudaStreamBeginCaptureToGraph(h->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  int rc = SMC_OK;
+  for (int par = 0; par < 2 && rc == SMC_OK; ++par) {
+    h->enq = (unsigned long long)par;
+    rc = enqueue_epoch(h);
+  }
+  set_condition_kernel<<<1, 32, 0, h->stream>>>(hdl, h->shards[0].ctrl, 0xFFFFFFF0u);
+  cudaGraph_t captured = nullptr;
+  cudaError_t e = cudaStreamEndCapture(h->stream, &captured);
+  h->stream = keep;
+  h->enq = keep_enq;
+  if (rc) return rc;
+  if (e != cudaSuccess) return fail(h, SMC_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+  CU(cudaGraphInstantiate(&h->graph_exec, h->graph, 0));
   return SMC_OK;
 }
 
@@ -728,6 +768,9 @@ void smc_destroy(smc_handle h) {
     cudaFree(s.ctrl); cudaFree(s.d_dst_planes[0]); cudaFree(s.d_dst_planes[1]); cudaFree(s.d_dst_anc);
   }
   cudaFree(h->d_table); cudaFree(h->d_recA); cudaFree(h->d_recB); cudaFree(h->d_barrier);
+  if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+  if (h->graph) cudaGraphDestroy(h->graph);
+  if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   if (h->h_ctrl) cudaFreeHost(h->h_ctrl);
   for (auto& e : h->ev) if (e) cudaEventDestroy(e);
   if (h->nccl && g_nccl.CommDestroy) g_nccl.CommDestroy(h->nccl);
@@ -746,6 +789,12 @@ int smc_set_stream(smc_handle h, void* s) {
     CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     h->own_stream = true;
   }
+  return SMC_OK;
+}
+
+int smc_set_graph(smc_handle h, int32_t on) {
+  if (!h) return fail(h, SMC_EINVAL, "NULL handle");
+  h->use_graph = on != 0;
   return SMC_OK;
 }
 
@@ -781,6 +830,17 @@ int smc_step(smc_handle h, int32_t* done) {
 int smc_run(smc_handle h) {
   int rc = check_ready(h);
   if (rc) return rc;
+  if (h->use_graph && !h->timing && h->comm != COMM_CALLBACK && !h->h_ctrl->done) {
+    // device-side epoch loop: one graph launch, one synchronisation
+    rc = build_graph(h);
+    if (rc) return rc;
+    h->started = true;
+    CU(cudaGraphLaunch(h->graph_exec, h->stream));
+    rc = read_ctrl(h);
+    if (rc) return rc;
+    h->enq = h->h_ctrl->epochs;
+    return status_of(*h->h_ctrl);
+  }
   int32_t done = 0;
   while (!done) {
     rc = smc_step(h, &done);

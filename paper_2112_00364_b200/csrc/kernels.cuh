@@ -48,6 +48,7 @@ struct Ctrl {
   unsigned long long first_err;      // ULLONG_MAX = none
   unsigned long long distinct;       // distinct ancestors in the last resample
   unsigned long long draws;          // uniforms drawn by propagation (all epochs)
+  unsigned long long seed;           // Philox key of the run (device-resident: graphs survive reset)
 };
 
 enum { ST_OK = 0, ST_REJECTED = 4, ST_NAN = 5, ST_OVERFLOW = 6 };
@@ -154,7 +155,6 @@ struct PropArgs {
   double* lw;                    // [n_local]
   unsigned long long n_local;    // also the plane stride
   unsigned long long shard_base; // global index of local particle 0
-  unsigned long long seed;
   RecA* recA;                    // gathered records, both parities [2][world]
   int world, rank;
   Ctrl* ctrl;
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kThreads) propagate_kernel(PropArgs a, ModelCo
     M::load(s, a.planes, a.n_local, i);
     if (M::pc(s) != kStop) {
       start_alive = 1;
-      Rng r(a.seed, (uint32_t)(a.shard_base + i), epoch);
+      Rng r(a.ctrl->seed, (uint32_t)(a.shard_base + i), epoch);
       for (;;) {
         const bool ck = M::step(s, lw, r, C, dg);
         if (ck || M::pc(s) == kStop) break;
@@ -240,7 +240,6 @@ struct ResArgs {
   unsigned long long n_local;         // particles in this shard (= plane stride)
   unsigned long long shard_base;
   unsigned long long n_total;
-  unsigned long long seed;
   int world, rank;
   RecA* recA;                         // [2][world]
   u128* recB;                         // [2][world] shard totals
@@ -287,12 +286,26 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(ResArgs a) {
   const Global G = read_global(a.recA + par * a.world, a.world);
   if (!G.ok) return;
   const unsigned long long base = (unsigned long long)blockIdx.x * kTile;
+  double v[kItems];
+  if (base + kTile <= a.n_local) {
+    // full tile: 16-byte loads, all issued before any math (MLP = kItems/2 per thread)
+    const double2* p = reinterpret_cast<const double2*>(a.lw + base);
+#pragma unroll
+    for (int r = 0; r < kItems / 2; ++r) {
+      const double2 t = __ldg(p + r * kThreads + threadIdx.x);
+      v[2 * r] = t.x;
+      v[2 * r + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+      const unsigned long long i = base + (unsigned long long)r * kThreads + threadIdx.x;
+      v[r] = i < a.n_local ? __ldg(a.lw + i) : -INFINITY;
+    }
+  }
   u128 acc = 0;
 #pragma unroll
-  for (int r = 0; r < kItems; ++r) {
-    const unsigned long long i = base + (unsigned long long)r * kThreads + threadIdx.x;
-    if (i < a.n_local) acc += quantize(__ldg(a.lw + i), G.m);
-  }
+  for (int r = 0; r < kItems; ++r) acc += quantize(v[r], G.m);
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) acc += shfl_xor_u128(acc, d);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -348,8 +361,8 @@ __device__ __forceinline__ Grid make_grid(const ResArgs& a, const u128* B, unsig
     if (g < a.rank) prefix += B[g];
     W += B[g];
   }
-  const uint4 r = philox4x32_10(make_uint4(0u, epoch, 0u, 1u), (uint32_t)a.seed,
-                                (uint32_t)(a.seed >> 32));
+  const unsigned long long seed = a.ctrl->seed;
+  const uint4 r = philox4x32_10(make_uint4(0u, epoch, 0u, 1u), (uint32_t)seed, (uint32_t)(seed >> 32));
   const unsigned long long z = hq_bits(r.x, r.y);
   Grid gr;
   gr.W = W;
@@ -510,6 +523,17 @@ __global__ void finalize_kernel(FinArgs a) {
 }
 
 // ============================================================================
+// whole-run CUDA graph: the WHILE node's condition = "not done"
+// ============================================================================
+__global__ void set_condition_kernel(cudaGraphConditionalHandle hdl, const Ctrl* c,
+                                     unsigned max_epochs) {
+  if (threadIdx.x == 0) {
+    const bool more = !c->done && c->epoch < max_epochs;
+    cudaGraphSetConditional(hdl, more ? 1u : 0u);
+  }
+}
+
+// ============================================================================
 // resampler-only helpers (BASELINE configs[4])
 // ============================================================================
 // Set the epoch and clear the records of a standalone resampling step.
@@ -536,12 +560,30 @@ __global__ void __launch_bounds__(kThreads) max_kernel(const double* lw, unsigne
   const unsigned par = c->epoch & 1;
   long long key = LLONG_MIN;
   bool bad = false;
-  for (unsigned long long i = (unsigned long long)blockIdx.x * kThreads + threadIdx.x; i < n;
-       i += (unsigned long long)gridDim.x * kThreads) {
-    const double v = __ldg(lw + i);
-    bad |= isnan(v) || v == INFINITY;
-    const long long k = order_key(v);
-    key = k > key ? k : key;
+  const unsigned long long n2 = n / 2;
+  const double2* p = reinterpret_cast<const double2*>(lw);
+  const unsigned long long stride = (unsigned long long)gridDim.x * kThreads;
+  unsigned long long i = (unsigned long long)blockIdx.x * kThreads + threadIdx.x;
+  for (; i + 3 * stride < n2; i += 4 * stride) {       // 4 x 16-byte loads in flight
+    double2 t[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) t[u] = __ldg(p + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      bad |= isnan(t[u].x) || t[u].x == INFINITY || isnan(t[u].y) || t[u].y == INFINITY;
+      const long long k0 = order_key(t[u].x), k1 = order_key(t[u].y);
+      key = max(key, max(k0, k1));
+    }
+  }
+  for (; i < n2; i += stride) {
+    const double2 t = __ldg(p + i);
+    bad |= isnan(t.x) || t.x == INFINITY || isnan(t.y) || t.y == INFINITY;
+    key = max(key, max(order_key(t.x), order_key(t.y)));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) {
+    const double t = __ldg(lw + n - 1);
+    bad |= isnan(t) || t == INFINITY;
+    key = max(key, order_key(t));
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {

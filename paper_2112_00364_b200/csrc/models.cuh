@@ -135,9 +135,15 @@ struct Crbd {
 // Planes: P0 {sigma, alpha} P1 {eps, lam} P2..P4 pending rates[6]
 //         P5 {pc, branch, sp, 0}.
 // ============================================================================
+// Rate guard: any lineage rate above kMaxRate (or not
+// finite) is outside the model's support -> weight -inf and the block ends
+// ("kill": branch index and pc advance, nothing else).
 struct Clads2 {
   static constexpr int kPlanes = 6;
   static constexpr int kPend = 6;
+  static constexpr double kMaxRate = 1e4;
+  __device__ static bool bad_rate(double r) { return !(r <= kMaxRate); }
+
   struct State { double sigma, alpha, eps, lam; double pend[kPend]; int pc, branch, sp; };
   __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
     uint4 v = ldp(P, st, 0, i); s.sigma = lo_d(v); s.alpha = hi_d(v);
@@ -193,9 +199,11 @@ struct Clads2 {
         if (d_bernoulli(r, pb)) {
           const double za = d_normal(r, 0.0, 1.0);
           const double zb = d_normal(r, 0.0, 1.0);
+          const double la = daughter(st, lam, za), lb = daughter(st, lam, zb);
+          if (bad_rate(la) || bad_rate(lb)) return 0;
           if (sp >= kStackCap) return -1;
-          stk_s[sp] = s; stk_l[sp] = daughter(st, lam, zb); ++sp;
-          lam = daughter(st, lam, za);
+          stk_s[sp] = s; stk_l[sp] = lb; ++sp;
+          lam = la;
           continue;
         }
         break;
@@ -225,8 +233,9 @@ struct Clads2 {
     const double tp = __ldg(b), tc = __ldg(b + 1);
     const bool internal = __ldg(b + 2) != 0.0;
     const bool first_left = __ldg(b + 3) != 0.0;
+    bool killed = bad_rate(s.lam);
     double t = tp;
-    for (;;) {
+    while (!killed) {
       const double dt = d_exp(r, s.lam);
       if (t - dt <= tc) {
         lw = lw + (-s.eps * s.lam * (t - tc));
@@ -236,26 +245,34 @@ struct Clads2 {
       t = t - dt;
       const double zs = d_normal(r, 0.0, 1.0);
       const double zc = d_normal(r, 0.0, 1.0);
-      const int u = undetected(t, daughter(s, s.lam, zs), s, rho, r);
+      const double ls = daughter(s, s.lam, zs);
+      if (bad_rate(ls)) { killed = true; break; }
+      const int u = undetected(t, ls, s, rho, r);
       if (u != 1) {
         if (u < 0) ++dg.overflow;
-        lw = -INFINITY;
+        killed = true;
         break;
       }
       lw = lw + kLn2;
       s.lam = daughter(s, s.lam, zc);
+      if (bad_rate(s.lam)) { killed = true; break; }
     }
-    if (internal) {
+    if (!killed && internal) {
       lw = lw + log(s.lam);
       const double zl = d_normal(r, 0.0, 1.0);
       const double zr = d_normal(r, 0.0, 1.0);
       const double rl = daughter(s, s.lam, zl), rr = daughter(s, s.lam, zr);
-      push(s, first_left ? rr : rl);
-      s.lam = first_left ? rl : rr;
-    } else {
+      if (bad_rate(rl) || bad_rate(rr)) {
+        killed = true;
+      } else {
+        push(s, first_left ? rr : rl);
+        s.lam = first_left ? rl : rr;
+      }
+    } else if (!killed) {
       lw = lw + log(rho);
       if (s.branch + 1 < C.n) s.lam = pop(s);
     }
+    if (killed) lw = -INFINITY;
     s.branch = s.branch + 1;
     s.pc = (s.branch == C.n) ? kStop : 1;
     return true;

@@ -203,3 +203,55 @@ def test_crbd_full_size_prefix(smc):
     """BASELINE configs[1] at 10^6 particles, first 4 epochs, element by element."""
     run_pair(smc, oracle.CRBD, inputs.tree("tree90"), inputs.CRBD_PARAMS, 1_000_000, 1,
              per_epoch=True, max_epochs=4)
+
+
+# ------------------------------------------------------------- whole-run CUDA graph
+@pytest.mark.parametrize("kind,data,params,N", [
+    (oracle.CRBD, "tree90", inputs.CRBD_PARAMS, 5000),
+    (oracle.GEOMETRIC, None, inputs.GEOMETRIC_PARAMS, 3001),     # particles stop at different epochs
+    (oracle.SEIR, "seir", None, 1500),
+    (oracle.CONSTW, None, inputs.CONSTW_PARAMS, 10),
+])
+def test_graph_run_matches_oracle(smc, kind, data, params, N):
+    if data == "tree90":
+        data = inputs.tree("tree90")
+    elif data == "seir":
+        data = inputs.seir_series()
+    g, o = both(smc, kind, data, params, N, 31)
+    rg = g.run_status()          # one graph launch (WHILE node)
+    ro = o.run()
+    assert rg == ro
+    if ro == oracle.EREJECTED:
+        assert g.log_z == -math.inf
+        return
+    assert g.log_z == pytest.approx(o.log_z, rel=RTOL)
+    compare(g, o)
+    sg, so = g.stats(), o.stats()
+    assert sg["epochs"] == so["epochs"] and sg["resamples"] == so["resamples"]
+    # a second sweep on the same handle after reset reuses the captured graph
+    g.reset(32)
+    o2 = oracle.Smc(kind, o._keep[0], params, N, 32)
+    assert g.run_status() == o2.run()
+    if math.isfinite(o2.log_z):
+        assert g.log_z == pytest.approx(o2.log_z, rel=RTOL)
+        compare(g, o2)
+
+
+def test_seir_all_rejected_agrees(smc):
+    # small N: every particle eventually has y_t > z_t -> EREJECTED on both sides
+    g, o = both(smc, oracle.SEIR, inputs.seir_series(), None, 700, 31)
+    assert g.run_status() == o.run() == oracle.EREJECTED
+    assert g.log_z == o.log_z == -math.inf
+    assert g.stats()["epochs"] == o.stats()["epochs"]
+
+
+def test_graph_and_step_modes_identical(smc):
+    m = smc.Model.clads2(inputs.tree("tree90"))
+    a = smc.Smc(m, 8192, 5)
+    a.run()
+    b = smc.Smc(m, 8192, 5)
+    b.set_graph(False)
+    b.run()
+    assert a.log_z == b.log_z
+    np.testing.assert_array_equal(a.log_weights(), b.log_weights())
+    np.testing.assert_array_equal(a.ancestors(), b.ancestors())
