@@ -363,6 +363,11 @@ def run_ours(args, wl):
         return
     r = bench_sweeps(args, wl, smc, torch, world, rank)
     N = r["N"]
+    # propagation roofline: uniforms drawn per second against the
+    # issue-rate ceiling 148 SM x 128 lanes x f_max / 34 instructions per uniform
+    f_max = float(pk.get("sm_max_mhz", 1965.0)) * 1e6
+    draw_peak = 148 * 128 * f_max / 34.0 / 1e9
+    draw_rate = r["draws"] / args.steps / max(r["prop_ms"] / args.steps * 1e-3, 1e-12) / 1e9
     # dominant kernel: propagation (ALU); resample chain: HBM
     prop_frac = r["prop_ms"] / max(r["prop_ms"] + r["res_ms"], 1e-9)
     line = dict(metric="particle-steps/s", value=r["value"], unit="particle-steps/s",
@@ -376,6 +381,10 @@ def run_ours(args, wl):
                 phase_ms=dict(propagate=r["prop_ms"] / args.steps, resample=r["res_ms"] / args.steps,
                               propagate_share=prop_frac),
                 draws_per_particle_step=r["draws"] / max(r["alive_steps"], 1),
+                roofline=dict(bound="alu", kernel=f"propagate_kernel<{wl['model']}>",
+                              achieved=draw_rate, peak=draw_peak, unit="Gdraws/s",
+                              frac=draw_rate / draw_peak, traffic=None,
+                              peak_source=f"derived: 148 SM x 128 lanes x {f_max/1e6:.0f} MHz / 34 instr per uniform (DESIGN.md s7)"),
                 gpu_launches=r["launches"], clocks=r["clocks"])
     if rank == 0 and not args.no_e2e and world == 1:
         e = e2e_sweeps(args, wl, smc, torch, N, min(args.steps, 3))
