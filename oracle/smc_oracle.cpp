@@ -464,6 +464,178 @@ struct Clads2Model {
   }
 };
 
+// ---- Lineage-keyed side trees (SURVEY c.2 #18) ------------
+// Every node of a hidden side tree (one lineage from its birth to its next
+// event) draws from its OWN Philox block: counter (id0, id1, n, TAG_NODE<<28 |
+// t), key = seed.  u0 = hq(B0,B1) times the event, u1 = hq(B2,B3) decides it.
+// A birth's two daughters get ids from the block with tag TAG_CHILD
+// (child a = (C0,C1), child b = (C2,C3)); ClaDS2 daughters' rate noises are the
+// Box-Muller pair of the block with tag TAG_Z.  The root of the k-th hidden
+// event of the branch has id (k, 0xFFFFFFFF).  "Undetected" is an AND over the
+// tree's nodes, so it does not depend on the order nodes are visited; the
+// oracle visits them depth-first.
+enum { TAG_NODE = 3, TAG_CHILD = 4, TAG_Z = 5 };
+const uint64_t SIDE_NODE_CAP = (1ull << 22);   // nodes per branch (all its side trees)
+
+Block side_block(uint64_t seed, uint32_t id0, uint32_t id1, uint32_t n, uint32_t t, uint32_t tag,
+                 uint64_t* draws) {
+  if (draws) *draws += 2;
+  return philox4x32_10(id0, id1, n, (tag << 28) | t, (uint32_t)seed, (uint32_t)(seed >> 32));
+}
+
+enum { SIDE_UNDETECTED = 0, SIDE_DETECTED = 1, SIDE_OVERFLOW = 2 };
+
+struct CrbdLRModel : CrbdModel {
+  uint64_t seed = 0;
+  mutable uint64_t* draws = nullptr;
+  // whole side tree of hidden event k born at age s0
+  int side_tree(uint32_t k, double s0, const State& st, uint32_t n, uint32_t t, uint64_t& count) const {
+    struct Node { uint32_t a, b; double s; };
+    std::vector<Node> stack;
+    stack.push_back(Node{k, 0xFFFFFFFFu, s0});
+    const double tot = st.lambda + st.mu;
+    const double pb = st.lambda / tot;
+    while (!stack.empty()) {
+      Node v = stack.back(); stack.pop_back();
+      if (++count > SIDE_NODE_CAP) return SIDE_OVERFLOW;
+      Block B = side_block(seed, v.a, v.b, n, t, TAG_NODE, draws);
+      double u0 = hq(B.v[0], B.v[1]), u1 = hq(B.v[2], B.v[3]);
+      double d = -std::log(u0) / tot;
+      if (d > v.s) {
+        if (u1 < rho) return SIDE_DETECTED;
+        continue;
+      }
+      double s2 = v.s - d;
+      if (u1 < pb) {
+        Block Cb = philox4x32_10(v.a, v.b, n, (TAG_CHILD << 28) | t, (uint32_t)seed, (uint32_t)(seed >> 32));
+        stack.push_back(Node{Cb.v[0], Cb.v[1], s2});
+        stack.push_back(Node{Cb.v[2], Cb.v[3], s2});
+      }
+    }
+    return SIDE_UNDETECTED;
+  }
+  int step_lr(State& s, double& lw, Stream& rs, uint64_t& overflow, uint32_t n, uint32_t t) const {
+    if (s.pc == 0) {
+      s.lambda = lam_fixed >= 0.0 ? lam_fixed : sample_gamma(rs, 1.0, 1.0);
+      s.mu = mu_fixed >= 0.0 ? mu_fixed : sample_gamma(rs, 1.0, 0.5);
+      s.branch = 0;
+      s.pc = 1;
+      return 0;
+    }
+    const Branch& b = br[s.branch];
+    lw = lw + (-s.mu * (b.tp - b.tc));
+    lw = lw + (b.internal ? std::log(s.lambda) : std::log(rho));
+    // hidden speciation times along the observed branch (the particle's own stream)
+    std::vector<double> ev;
+    double tt = b.tp;
+    for (;;) {
+      tt = tt - sample_exp(rs, s.lambda);
+      if (tt <= b.tc) break;
+      ev.push_back(tt);
+    }
+    uint64_t count = 0;
+    bool dead = false;
+    for (size_t k = 0; k < ev.size() && !dead; ++k) {
+      int r = side_tree((uint32_t)k, ev[k], s, n, t, count);
+      if (r != SIDE_UNDETECTED) {
+        if (r == SIDE_OVERFLOW) ++overflow;
+        dead = true;
+      }
+    }
+    if (dead) lw = -INFINITY;
+    else for (size_t k = 0; k < ev.size(); ++k) lw = lw + LN2;
+    s.branch = s.branch + 1;
+    s.pc = (s.branch == (int)br.size()) ? PC_STOP : 1;
+    return 1;
+  }
+};
+
+struct Clads2LRModel : Clads2Model {
+  uint64_t seed = 0;
+  mutable uint64_t* draws = nullptr;
+  int side_tree(uint32_t k, double s0, double lam0, const State& st, uint32_t n, uint32_t t,
+                uint64_t& count) const {
+    struct Node { uint32_t a, b; double s, lam; };
+    std::vector<Node> stack;
+    stack.push_back(Node{k, 0xFFFFFFFFu, s0, lam0});
+    const double pb = 1.0 / (1.0 + st.eps);
+    while (!stack.empty()) {
+      Node v = stack.back(); stack.pop_back();
+      if (++count > SIDE_NODE_CAP) return SIDE_OVERFLOW;
+      Block B = side_block(seed, v.a, v.b, n, t, TAG_NODE, draws);
+      double u0 = hq(B.v[0], B.v[1]), u1 = hq(B.v[2], B.v[3]);
+      double d = -std::log(u0) / (v.lam * (1.0 + st.eps));
+      if (d > v.s) {
+        if (u1 < rho) return SIDE_DETECTED;
+        continue;
+      }
+      double s2 = v.s - d;
+      if (u1 < pb) {
+        Block Z = side_block(seed, v.a, v.b, n, t, TAG_Z, draws);
+        double r = std::sqrt(-2.0 * std::log(hq(Z.v[0], Z.v[1])));
+        double th = TWO_PI * hq(Z.v[2], Z.v[3]);
+        double za = r * std::cos(th), zb = r * std::sin(th);
+        double la = daughter(st, v.lam, za), lb = daughter(st, v.lam, zb);
+        if (bad_rate(la) || bad_rate(lb)) return SIDE_DETECTED;   // rate guard: reject
+        Block Cb = philox4x32_10(v.a, v.b, n, (TAG_CHILD << 28) | t, (uint32_t)seed, (uint32_t)(seed >> 32));
+        stack.push_back(Node{Cb.v[0], Cb.v[1], s2, la});
+        stack.push_back(Node{Cb.v[2], Cb.v[3], s2, lb});
+      }
+    }
+    return SIDE_UNDETECTED;
+  }
+  int step_lr(State& s, double& lw, Stream& rs, uint64_t& overflow, uint32_t n, uint32_t t) const {
+    if (s.pc == 0) return step(s, lw, rs, overflow);        // INIT + root split (main stream)
+    const Branch& b = br[s.branch];
+    if (bad_rate(s.lam)) return kill(s, lw);
+    struct Root { double s, lam; };
+    std::vector<Root> roots;
+    double tt = b.tp;
+    for (;;) {
+      double dt = sample_exp(rs, s.lam);
+      if (tt - dt <= b.tc) {
+        lw = lw + (-s.eps * s.lam * (tt - b.tc));
+        break;
+      }
+      lw = lw + (-s.eps * s.lam * dt);
+      tt = tt - dt;
+      double zs = sample_normal(rs, 0.0, 1.0);
+      double zc = sample_normal(rs, 0.0, 1.0);
+      double ls = daughter(s, s.lam, zs);
+      if (bad_rate(ls)) return kill(s, lw);
+      roots.push_back(Root{tt, ls});
+      s.lam = daughter(s, s.lam, zc);
+      if (bad_rate(s.lam)) return kill(s, lw);
+    }
+    if (b.internal) {
+      lw = lw + std::log(s.lam);
+      double zl = sample_normal(rs, 0.0, 1.0);
+      double zr = sample_normal(rs, 0.0, 1.0);
+      double rl = daughter(s, s.lam, zl), rr = daughter(s, s.lam, zr);
+      if (bad_rate(rl) || bad_rate(rr)) return kill(s, lw);
+      s.pend[s.sp++] = b.first_left ? rr : rl;
+      s.lam = b.first_left ? rl : rr;
+    } else {
+      lw = lw + std::log(rho);
+      if (s.branch + 1 < (int)br.size()) s.lam = s.pend[--s.sp];
+    }
+    uint64_t count = 0;
+    bool dead = false;
+    for (size_t k = 0; k < roots.size() && !dead; ++k) {
+      int r = side_tree((uint32_t)k, roots[k].s, roots[k].lam, s, n, t, count);
+      if (r != SIDE_UNDETECTED) {
+        if (r == SIDE_OVERFLOW) ++overflow;
+        dead = true;
+      }
+    }
+    if (dead) lw = -INFINITY;
+    else for (size_t k = 0; k < roots.size(); ++k) lw = lw + LN2;
+    s.branch = s.branch + 1;
+    s.pc = (s.branch == (int)br.size()) ? PC_STOP : 1;
+    return 1;
+  }
+};
+
 // ---- Vector-borne disease SEIR --------------
 struct SeirParams { double lam_h, del_h, gam_h, lam_m, del_m, rho; };
 struct SeirCounts { int64_t sh, eh, ih, rh, sm, em, im; };
@@ -714,12 +886,31 @@ struct SmcBase {
   ResampleOut last{};
 };
 
+inline void set_side_draws(...) {}
+inline void set_side_draws(CrbdLRModel& m, uint64_t* d) { m.draws = d; }
+inline void set_side_draws(Clads2LRModel& m, uint64_t* d) { m.draws = d; }
+
+// Adapter: the Alg. 1 loop calls step(); lineage-keyed models need (n, t).
+template <class M> struct StepCall {
+  static int call(const M& m, typename M::State& s, double& lw, Stream& rs, uint64_t& ovf,
+                  uint32_t, uint32_t) { return m.step(s, lw, rs, ovf); }
+};
+template <> struct StepCall<CrbdLRModel> {
+  static int call(const CrbdLRModel& m, CrbdLRModel::State& s, double& lw, Stream& rs,
+                  uint64_t& ovf, uint32_t n, uint32_t t) { return m.step_lr(s, lw, rs, ovf, n, t); }
+};
+template <> struct StepCall<Clads2LRModel> {
+  static int call(const Clads2LRModel& m, Clads2LRModel::State& s, double& lw, Stream& rs,
+                  uint64_t& ovf, uint32_t n, uint32_t t) { return m.step_lr(s, lw, rs, ovf, n, t); }
+};
+
 template <class M>
 struct Smc : SmcBase {
   M model;
   std::vector<typename M::State> st, tmp;
   Smc(const M& m, uint64_t n, uint64_t s) : model(m) {
     N = n; seed = s;
+    set_side_draws(model, &draws);
     st.assign(N, typename M::State());
     lw.assign(N, 0.0);
     anc.resize(N);
@@ -738,7 +929,7 @@ struct Smc : SmcBase {
       ++alive_steps;
       Stream rs = make_stream(seed, (uint32_t)n, t, TAG_PARTICLE, &draws);
       for (;;) {
-        int ckpt = model.step(st[n], lw[n], rs, overflow);
+        int ckpt = StepCall<M>::call(model, st[n], lw[n], rs, overflow, (uint32_t)n, t);
         if (ckpt || st[n].pc == PC_STOP) break;
       }
     }
@@ -795,7 +986,8 @@ thread_local std::string g_err;
 // =============================================================================
 extern "C" {
 
-enum { K_CRBD = 1, K_CLADS2 = 2, K_SEIR = 3, K_GEOMETRIC = 10, K_SSM = 11, K_CONSTW = 12 };
+enum { K_CRBD = 1, K_CLADS2 = 2, K_SEIR = 3, K_CRBD_LR = 4, K_CLADS2_LR = 5,
+       K_GEOMETRIC = 10, K_SSM = 11, K_CONSTW = 12 };
 
 const char* oracle_errmsg() { return g_err.c_str(); }
 
@@ -914,6 +1106,29 @@ void* oracle_smc_create(int kind, const double* data, uint64_t data_len,
       m.rho = P(0, 1.0); m.lam0_fixed = P(1, -1.0); m.sigma_fixed = P(2, -1.0);
       m.alpha_fixed = P(3, -1.0); m.eps_fixed = P(4, -1.0);
       return new Smc<Clads2Model>(m, N, seed);
+    }
+    case K_CRBD_LR: {
+      bool ok; Tree T = parse_tree(data, data_len, ok);
+      if (!ok) { g_err = "bad tree"; return nullptr; }
+      CrbdLRModel m;
+      preorder_left(T, T.root, m.br);
+      m.rho = P(0, 1.0); m.lam_fixed = P(1, -1.0); m.mu_fixed = P(2, -1.0);
+      m.seed = seed;
+      return new Smc<CrbdLRModel>(m, N, seed);
+    }
+    case K_CLADS2_LR: {
+      bool ok; Tree T = parse_tree(data, data_len, ok);
+      if (!ok) { g_err = "bad tree"; return nullptr; }
+      Clads2LRModel m;
+      int maxpend = 0;
+      preorder_smaller(T, T.root, m.br, maxpend, 0);
+      if (maxpend > Clads2Model::PEND) { g_err = "pending-rate stack exceeds 6"; return nullptr; }
+      int l = T.left[T.root], r = T.right[T.root];
+      m.root_first_left = T.ntips(l) <= T.ntips(r);
+      m.rho = P(0, 1.0); m.lam0_fixed = P(1, -1.0); m.sigma_fixed = P(2, -1.0);
+      m.alpha_fixed = P(3, -1.0); m.eps_fixed = P(4, -1.0);
+      m.seed = seed;
+      return new Smc<Clads2LRModel>(m, N, seed);
     }
     case K_SEIR: {
       SeirModel m;

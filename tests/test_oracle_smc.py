@@ -117,25 +117,41 @@ def test_ssm_vs_kalman():
     mean_ratio_within_3se(lz, ref)
 
 
-def test_crbd_fixed_rates_unbiased():
-    ref = cf.crbd_log_lik(TREE5, 0.3, 0.1)
-    lz = [run(oracle.CRBD, oracle.tree_blob(TREE5), [1.0, 0.3, 0.1], 1000, s)[0].log_z
+CRBD_KINDS = pytest.mark.parametrize("kind", [oracle.CRBD, oracle.CRBD_LR], ids=["seq", "lineage"])
+
+
+@CRBD_KINDS
+@pytest.mark.parametrize("lam,mu", [(0.3, 0.1), (0.25, 0.25), (0.2, 0.4)])
+def test_crbd_fixed_rates_unbiased(kind, lam, mu):
+    ref = cf.crbd_log_lik(TREE5, lam, mu)
+    lz = [run(kind, oracle.tree_blob(TREE5), [1.0, lam, mu], 1000, s)[0].log_z
           for s in range(1, 101)]
     mean_ratio_within_3se(lz, ref)
 
 
-def test_crbd_yule_unbiased():
+@CRBD_KINDS
+def test_crbd_yule_unbiased(kind):
     ref = cf.crbd_log_lik(TREE5, 0.5, 0.0)
-    lz = [run(oracle.CRBD, oracle.tree_blob(TREE5), [1.0, 0.5, 0.0], 1000, s)[0].log_z
+    lz = [run(kind, oracle.tree_blob(TREE5), [1.0, 0.5, 0.0], 1000, s)[0].log_z
           for s in range(1, 101)]
     mean_ratio_within_3se(lz, ref)
 
 
-def test_crbd_priors_unbiased():
+@CRBD_KINDS
+def test_crbd_priors_unbiased(kind):
     g = json.load(open(os.path.join(GOLD, "crbd_values.json")))
-    lz = [run(oracle.CRBD, oracle.tree_blob(TREE5), inputs.CRBD_PARAMS, 1000, s)[0].log_z
+    lz = [run(kind, oracle.tree_blob(TREE5), inputs.CRBD_PARAMS, 1000, s)[0].log_z
           for s in range(1, 101)]
     mean_ratio_within_3se(lz, g["logZ_priors_gamma11_gamma1_0.5"])
+
+
+@CRBD_KINDS
+def test_crbd_rho_half_unbiased(kind):
+    # incomplete sampling (rho = 0.5): exercises the survivor Bernoulli branch
+    ref = cf.crbd_log_lik(TREE5, 0.3, 0.1, rho=0.5)
+    lz = [run(kind, oracle.tree_blob(TREE5), [0.5, 0.3, 0.1], 1000, s)[0].log_z
+          for s in range(1, 101)]
+    mean_ratio_within_3se(lz, ref)
 
 
 def test_crbd_epochs_and_draws():
@@ -147,17 +163,19 @@ def test_crbd_epochs_and_draws():
     assert np.all(f[:, 0] == -1) and np.all(f[:, 1] == 8)
 
 
-def test_clads2_reduces_to_crbd():
+@pytest.mark.parametrize("kind", [oracle.CLADS2, oracle.CLADS2_LR], ids=["seq", "lineage"])
+def test_clads2_reduces_to_crbd(kind):
     # sigma = 0, alpha = 1, lambda0 = 0.3, eps = 1/3  ==  CRBD(0.3, 0.1)
     ref = cf.crbd_log_lik(TREE5, 0.3, 0.1)
-    lz = [run(oracle.CLADS2, oracle.tree_blob(TREE5), [1.0, 0.3, 0.0, 1.0, 1 / 3], 1000, s)[0].log_z
+    lz = [run(kind, oracle.tree_blob(TREE5), [1.0, 0.3, 0.0, 1.0, 1 / 3], 1000, s)[0].log_z
           for s in range(1, 101)]
     mean_ratio_within_3se(lz, ref)
 
 
-def test_clads2_priors_runs():
+@pytest.mark.parametrize("kind", [oracle.CLADS2, oracle.CLADS2_LR], ids=["seq", "lineage"])
+def test_clads2_priors_runs(kind):
     t90 = inputs.tree("tree90")
-    s, rc = run(oracle.CLADS2, oracle.tree_blob(t90), inputs.CLADS2_PARAMS, 200, 2)
+    s, rc = run(kind, oracle.tree_blob(t90), inputs.CLADS2_PARAMS, 200, 2)
     assert rc == oracle.OK and np.isfinite(s.log_z)
     st = s.stats()
     assert st["epochs"] == 178
