@@ -105,11 +105,14 @@ def dist_init(gpus):
     return world, rank, local
 
 
-def model_for(smc, wl):
+RNG = {"lineage": True, "sequential": False}
+
+
+def model_for(smc, wl, rng="lineage"):
     if wl["model"] == "crbd":
-        return smc.Model.crbd(inputs.tree(wl["tree"]), inputs.CRBD_PARAMS)
+        return smc.Model.crbd(inputs.tree(wl["tree"]), inputs.CRBD_PARAMS, lineage=RNG[rng])
     if wl["model"] == "clads2":
-        return smc.Model.clads2(inputs.tree(wl["tree"]), inputs.CLADS2_PARAMS)
+        return smc.Model.clads2(inputs.tree(wl["tree"]), inputs.CLADS2_PARAMS, lineage=RNG[rng])
     if wl["model"] == "seir":
         return smc.Model.seir(inputs.seir_series())
     raise ValueError(wl)
@@ -121,7 +124,9 @@ def oracle_sweep_rate(wl, budget_s=15.0, n_cap=None):
     sweep of the same model with n particles, n chosen so the run takes
     roughly budget_s.  Returns (particle-steps/s, sample description, seconds)."""
     import oracle
-    kind = {"crbd": oracle.CRBD, "clads2": oracle.CLADS2, "seir": oracle.SEIR}[wl["model"]]
+    lin = getattr(oracle_sweep_rate, "rng", "lineage") == "lineage"
+    kind = {"crbd": oracle.CRBD_LR if lin else oracle.CRBD,
+            "clads2": oracle.CLADS2_LR if lin else oracle.CLADS2, "seir": oracle.SEIR}[wl["model"]]
     if wl["model"] in ("crbd", "clads2"):
         data = oracle.tree_blob(inputs.tree(wl["tree"]))
         params = inputs.CRBD_PARAMS if wl["model"] == "crbd" else inputs.CLADS2_PARAMS
@@ -183,7 +188,7 @@ def run_reference(args, wl):
         line = dict(metric="particle-steps/s", value=v, unit="particle-steps/s", impl="reference")
     line.update(n_gpus=world, steps=args.steps, warmup=args.warmup, higher_is_better=True,
                 scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
-                config=dict(workload=args.workload, desc=wl["desc"]),
+                config=dict(workload=args.workload, desc=wl["desc"], rng=args.rng),
                 cpu_baseline=dict(value=v, unit=line["unit"], cores=ncores, kind="oracle",
                                   sample=sample),
                 e2e=dict(value=v, unit=line["unit"], h2d_bytes_per_step=0, d2h_bytes_per_step=0))
@@ -193,7 +198,7 @@ def run_reference(args, wl):
 # ----------------------------------------------------------------------------- our arm
 def bench_sweeps(args, wl, smc, torch, world, rank):
     N = args.n or wl["n"]
-    model = model_for(smc, wl)
+    model = model_for(smc, wl, args.rng)
     stream = torch.cuda.current_stream()
     if world == 1:
         h = smc.Smc(model, N, seed=1, stream=stream)
@@ -259,7 +264,7 @@ def e2e_sweeps(args, wl, smc, torch, N, k_steps):
     """End to end through the public API with host buffers: every step creates a
     handle from the host model description (H2D of the tree table), runs the
     sweep, and reads back log Z and the N final log-weights (D2H)."""
-    model = model_for(smc, wl)
+    model = model_for(smc, wl, args.rng)
     ts = []
     h2d = model.data.nbytes + model.params.nbytes
     for k in range(k_steps + 1):
@@ -375,13 +380,16 @@ def run_ours(args, wl):
                 ms_per_step=r["t_ms"] / args.steps, higher_is_better=True, scaling="weak",
                 vs_baseline=None, dtype="f64", data="synthetic",
                 config=dict(workload=args.workload, desc=wl["desc"], n_per_gpu=N,
+                            rng=args.rng if wl["model"] in ("crbd", "clads2") else "sequential",
                             epochs_per_sweep=r["epochs"] // args.steps,
                             l2="flushed between steps (state fits L2 within a sweep)"),
                 sweeps_per_s=r["sweeps"], mean_log_z=r["logz"],
                 phase_ms=dict(propagate=r["prop_ms"] / args.steps, resample=r["res_ms"] / args.steps,
                               propagate_share=prop_frac),
                 draws_per_particle_step=r["draws"] / max(r["alive_steps"], 1),
-                roofline=dict(bound="alu", kernel=f"propagate_kernel<{wl['model']}>",
+                roofline=dict(bound="alu",
+                              kernel=("propagate_lr_kernel" if args.rng == "lineage" and wl["model"] != "seir"
+                                      else "propagate_kernel") + f"<{wl['model']}>",
                               achieved=draw_rate, peak=draw_peak, unit="Gdraws/s",
                               frac=draw_rate / draw_peak, traffic=None,
                               peak_source=f"derived: 148 SM x 128 lanes x {f_max/1e6:.0f} MHz / 34 instr per uniform (DESIGN.md s7)"),
@@ -407,6 +415,9 @@ def main():
     ap.add_argument("--workload", default="crbd", choices=sorted(WORKLOADS))
     ap.add_argument("--n", type=int, default=0, help="particles per GPU (default: workload's)")
     ap.add_argument("--sigma", type=float, default=1.0, help="resample workload: lw ~ sigma N(0,1)")
+    ap.add_argument("--rng", default="lineage", choices=sorted(RNG),
+                    help="tree models: lineage-keyed side trees (DESIGN R-18, cooperative kernel) "
+                         "or the sequential per-particle stream (R-11)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
@@ -416,6 +427,7 @@ def main():
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 breaks the timing rules", file=sys.stderr)
     wl = WORKLOADS[args.workload]
+    oracle_sweep_rate.rng = args.rng
     if args.impl == "reference":
         run_reference(args, wl)
     else:

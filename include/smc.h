@@ -67,6 +67,11 @@ typedef enum {
 } smc_model_kind;
 
 #define SMC_FLAG_STRICT 1u   /* helper-stack overflow is an error instead of weight -inf */
+/* CRBD / CLADS2: lineage-keyed side trees: every hidden-tree
+ * node draws from its own Philox counter, so a CTA evaluates one particle's
+ * side trees in parallel (cooperative kernel).  Same model, different (equally
+ * valid) stream layout; results match the oracle's lineage-keyed kinds. */
+#define SMC_FLAG_LINEAGE_RNG 2u
 
 /*
  * Model description (all arrays COPIED at create).
@@ -113,6 +118,9 @@ typedef struct {
   double ms_propagate;              /* CUDA-event time of propagation (smc_set_timing on)    */
   double ms_resample;               /* ... of the resampling chain (reduce, gather, finalize) */
   uint64_t timed_epochs;            /* epochs covered by the two timers                      */
+  uint64_t side_roots;              /* lineage-keyed kernels: hidden events (side-tree roots) */
+  uint32_t max_rounds;              /* ... longest cooperative phase of a batch (rounds)      */
+  uint32_t max_side_nodes;          /* ... largest side-tree node count of one particle-step  */
 } smc_stats_t;
 
 /* --- lifetime --------------------------------------------------------------- */

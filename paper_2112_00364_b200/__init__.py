@@ -27,6 +27,7 @@ _lib = C.CDLL(_LIB_PATH, mode=C.RTLD_GLOBAL)
 OK, EINVAL, ECUDA, ENCCL, EREJECTED, ENAN, EOVERFLOW, ESTATE = range(8)
 CRBD, CLADS2, SEIR, GEOMETRIC, SSM, CONSTW, RESAMPLE_BENCH = 1, 2, 3, 10, 11, 12, 20
 FLAG_STRICT = 1
+FLAG_LINEAGE_RNG = 2
 
 FIELDS = {
     CRBD: ["pc", "branch", "lambda", "mu"],
@@ -53,7 +54,8 @@ class smc_stats_t(C.Structure):
                 ("status", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
                 ("shards", C.c_int32), ("state_bytes", C.c_uint32), ("done", C.c_uint32),
                 ("draws", C.c_uint64), ("ms_propagate", C.c_double), ("ms_resample", C.c_double),
-                ("timed_epochs", C.c_uint64)]
+                ("timed_epochs", C.c_uint64), ("side_roots", C.c_uint64),
+                ("max_rounds", C.c_uint32), ("max_side_nodes", C.c_uint32)]
 
 
 ALLGATHER_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)
@@ -157,12 +159,12 @@ class Model:
                            _dptr(self.params), self.params.size, flags)
 
     @staticmethod
-    def crbd(tree, params=(1.0, -1.0, -1.0), flags=0):
-        return Model(CRBD, tree_data(tree), params, flags=flags)
+    def crbd(tree, params=(1.0, -1.0, -1.0), flags=0, lineage=False):
+        return Model(CRBD, tree_data(tree), params, flags=flags | (FLAG_LINEAGE_RNG if lineage else 0))
 
     @staticmethod
-    def clads2(tree, params=(1.0, -1.0, -1.0, -1.0, -1.0), flags=0):
-        return Model(CLADS2, tree_data(tree), params, flags=flags)
+    def clads2(tree, params=(1.0, -1.0, -1.0, -1.0, -1.0), flags=0, lineage=False):
+        return Model(CLADS2, tree_data(tree), params, flags=flags | (FLAG_LINEAGE_RNG if lineage else 0))
 
     @staticmethod
     def seir(y, params=None):

@@ -41,6 +41,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         nvcc = "/usr/local/cuda/bin/nvcc"
     cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
            "-o", LIB + ".tmp", SRC]
+    extra = os.environ.get("SMC_NVCC_FLAGS", "").split()
+    cmd[1:1] = extra
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)

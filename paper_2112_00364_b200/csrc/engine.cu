@@ -22,6 +22,7 @@
 
 #include "smc.h"
 #include "kernels.cuh"
+#include "lineage.cuh"
 
 using namespace smc;
 
@@ -80,6 +81,9 @@ enum CommKind { COMM_LOCAL = 0, COMM_NCCL = 1, COMM_CALLBACK = 2 };
 
 struct smc_ctx {
   int kind = 0;
+  bool lineage = false;           // §R-18 lineage-keyed side trees (SMC_FLAG_LINEAGE_RNG)
+  int lr_grid = 0;                // persistent grid of the cooperative kernel
+  TaskArrays tasks{};
   int planes = 0;                 // 16-byte planes per particle
   uint32_t flags = 0;
   unsigned long long n_per = 0;   // particles per shard
@@ -221,6 +225,7 @@ int setup_model(smc_ctx* h, const smc_model* m) {
   if (!m) return fail(h, SMC_EINVAL, "model is NULL");
   h->kind = m->kind;
   h->flags = m->flags;
+  h->lineage = (m->flags & SMC_FLAG_LINEAGE_RNG) && (m->kind == SMC_CRBD || m->kind == SMC_CLADS2);
   for (int i = 0; i < 12; ++i) h->mc.p[i] = 0.0;
   auto P = [&](int i, double dflt) { return (m->params && i < m->n_params) ? m->params[i] : dflt; };
   std::string err;
@@ -392,6 +397,24 @@ int common_init(smc_ctx* h, const smc_model* m, unsigned long long n_per, int wo
   CU(cudaMalloc(&h->d_recB, 2 * world * sizeof(u128)));
   CU(cudaMalloc(&h->d_barrier, sizeof(int)));
   CU(cudaMallocHost(&h->h_ctrl, sizeof(Ctrl)));
+  if (h->lineage) {
+    int per_sm = 0;
+    if (h->kind == SMC_CRBD)
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, propagate_lr_kernel<CrbdLR>, kLRThreads, 0));
+    else
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, propagate_lr_kernel<Clads2LR>, kLRThreads, 0));
+    int dev = 0, sms = 0;
+    CU(cudaGetDevice(&dev));
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const unsigned long long batches = (n_per + kLRThreads - 1) / kLRThreads;
+    h->lr_grid = (int)std::min<unsigned long long>(batches, (unsigned long long)std::max(1, per_sm) * sms);
+    h->tasks.cap = kTasksPerCta;
+    const size_t nt = (size_t)h->lr_grid * h->tasks.cap;
+    CU(cudaMalloc(&h->tasks.s, nt * sizeof(double)));
+    if (h->kind == SMC_CLADS2) CU(cudaMalloc(&h->tasks.lam, nt * sizeof(double)));
+    CU(cudaMalloc(&h->tasks.id, nt * sizeof(unsigned long long)));
+    CU(cudaMalloc(&h->tasks.owner, nt * sizeof(unsigned short)));
+  }
   h->shards.resize(n_local_shards);
   for (int i = 0; i < n_local_shards; ++i) {
     Shard& s = h->shards[i];
@@ -454,7 +477,27 @@ void launch_prop(smc_ctx* h, Shard& s, int cur) {
   const unsigned grid = (unsigned)((h->n_per + kThreads - 1) / kThreads);
   propagate_kernel<M><<<grid, kThreads, 0, h->stream>>>(a, h->mc);
 }
+template <class M>
+void launch_prop_lr(smc_ctx* h, Shard& s, int cur) {
+  LRArgs a;
+  a.p.planes = s.planes[cur];
+  a.p.lw = s.lw;
+  a.p.n_local = h->n_per;
+  a.p.shard_base = s.base;
+  a.p.recA = h->d_recA;
+  a.p.world = h->world;
+  a.p.rank = s.id;
+  a.p.ctrl = s.ctrl;
+  a.t = h->tasks;
+  a.n_batches = (unsigned)((h->n_per + kLRThreads - 1) / kLRThreads);
+  propagate_lr_kernel<M><<<h->lr_grid, kLRThreads, 0, h->stream>>>(a, h->mc);
+}
 void launch_propagate(smc_ctx* h, Shard& s, int cur) {
+  if (h->lineage) {
+    if (h->kind == SMC_CRBD) launch_prop_lr<CrbdLR>(h, s, cur);
+    else launch_prop_lr<Clads2LR>(h, s, cur);
+    return;
+  }
   switch (h->kind) {
     case SMC_CRBD: launch_prop<Crbd>(h, s, cur); break;
     case SMC_CLADS2: launch_prop<Clads2>(h, s, cur); break;
@@ -768,6 +811,7 @@ void smc_destroy(smc_handle h) {
     cudaFree(s.ctrl); cudaFree(s.d_dst_planes[0]); cudaFree(s.d_dst_planes[1]); cudaFree(s.d_dst_anc);
   }
   cudaFree(h->d_table); cudaFree(h->d_recA); cudaFree(h->d_recB); cudaFree(h->d_barrier);
+  cudaFree(h->tasks.s); cudaFree(h->tasks.lam); cudaFree(h->tasks.id); cudaFree(h->tasks.owner);
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
   if (h->graph) cudaGraphDestroy(h->graph);
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
@@ -925,17 +969,22 @@ int smc_stats(smc_handle h, smc_stats_t* out) {
   out->ms_resample = h->ms_resample;
   out->timed_epochs = h->timed_epochs;
   if (h->stream && cudaStreamSynchronize(h->stream) == cudaSuccess) {
-    unsigned long long alive = 0, ovf = 0, fe = ~0ull, drw = 0;
+    unsigned long long alive = 0, ovf = 0, fe = ~0ull, drw = 0, roots = 0;
+    unsigned mr = 0, mn = 0;
     for (auto& s : h->shards) {
       Ctrl c;
       if (cudaMemcpy(&c, s.ctrl, sizeof(c), cudaMemcpyDeviceToHost) != cudaSuccess) break;
       alive += c.alive_steps; ovf += c.overflow; fe = std::min(fe, c.first_err); drw += c.draws;
+      roots += c.side_roots; mr = std::max(mr, c.max_rounds); mn = std::max(mn, c.max_side_nodes);
       out->epochs = c.epochs; out->resamples = c.resamples; out->done = c.done;
       if (c.status && !out->status) out->status = status_of(c);
     }
     out->alive_particle_steps = alive;
     out->overflow = ovf;
     out->draws = drw;
+    out->side_roots = roots;
+    out->max_rounds = mr;
+    out->max_side_nodes = mn;
     out->first_error_particle = fe == ~0ull ? -1 : (int64_t)fe;
   }
   return SMC_OK;

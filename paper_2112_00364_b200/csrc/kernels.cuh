@@ -49,6 +49,11 @@ struct Ctrl {
   unsigned long long distinct;       // distinct ancestors in the last resample
   unsigned long long draws;          // uniforms drawn by propagation (all epochs)
   unsigned long long seed;           // Philox key of the run (device-resident: graphs survive reset)
+  unsigned batch;                    // next 256-particle batch (persistent propagation grids)
+  unsigned max_rounds;               // diag: longest cooperative phase (rounds) in a batch
+  unsigned long long side_roots;     // diag: hidden events (side-tree roots) generated
+  unsigned max_side_nodes;           // diag: largest per-particle side-tree node count
+  unsigned pad_;
 };
 
 enum { ST_OK = 0, ST_REJECTED = 4, ST_NAN = 5, ST_OVERFLOW = 6 };
@@ -488,7 +493,7 @@ __global__ void finalize_kernel(FinArgs a) {
   const unsigned par = epoch & 1;
   const Global G = read_global(a.recA + par * a.world, a.world);
   if (G.flags) {
-    c->status = ST_NAN;
+    c->status = (G.flags & 1u) ? ST_NAN : ST_OVERFLOW;   // bit 1: side-tree task stack full
     c->done = 1;
     c->epochs = c->epochs + 1;
   } else if (!(G.m > -INFINITY)) {
@@ -514,6 +519,7 @@ __global__ void finalize_kernel(FinArgs a) {
       c->epoch = epoch + 1;
     }
   }
+  c->batch = 0;
   // reset this shard's records of the other parity for the next epoch
   RecA* nx = a.recA + (par ^ 1) * a.world + a.rank;
   nx->key = LLONG_MIN;

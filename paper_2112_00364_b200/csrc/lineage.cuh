@@ -1,0 +1,473 @@
+// lineage.cuh — cooperative propagation for the birth-death models under the
+// lineage-keyed side-tree reading (SURVEY c.2 #18).
+//
+// The cost of CRBD / ClaDS2 propagation is the "goes undetected" simulation of
+// hidden side trees ("recursive and stochastic tree constructions").
+// Its size is heavy-tailed: in early epochs one particle's tree can hold 10^5
+// nodes, and with one thread per particle that single thread bounds the whole
+// epoch.  Under §R-18 every tree node draws from its own Philox block (counter
+// = node id, particle, epoch, tag), so a tree's nodes can be evaluated in any
+// order.  This kernel therefore runs, per CTA, a batch of 256 particles:
+//   phase 1  each thread walks its particle's observed branch on the
+//            particle's own stream (INIT, hidden event times, node bookkeeping)
+//            and pushes one root task per hidden event onto the CTA's stack;
+//   phase 2  rounds: every particle ("owner") with pending tasks gets W =
+//            256 / (#owners with tasks) lanes (its top W tasks, LIFO per
+//            owner); lanes left over take tasks from a CTA overflow stack.
+//            With many busy owners each explores depth-first (the order a
+//            sequential DFS uses, so a supercritical tree is detected along
+//            one path instead of 256); when few remain, their trees get the
+//            idle lanes.  Tasks of particles already detected are pruned;
+//   phase 3  each thread finishes its particle: -inf if any node was detected
+//            (or the node cap was exceeded), else + ln 2 per hidden event.
+// The grid is persistent (CTAs pull 256-particle batches from a counter), so a
+// CTA stuck on a giant tree does not hold back the other batches, and the giant
+// tree itself is explored 256 nodes at a time.
+#pragma once
+#include "kernels.cuh"
+
+namespace smc {
+
+#ifndef SMC_LR_THREADS
+#define SMC_LR_THREADS 128
+#endif
+#ifndef SMC_LR_MINB
+#define SMC_LR_MINB 8
+#endif
+constexpr int kLRThreads = SMC_LR_THREADS;     // particles (owners) per batch = threads per CTA
+constexpr unsigned kSideNodeCap = 1u << 22;      // nodes per branch (all its side trees)
+constexpr int kSeg = 512;                        // per-owner LIFO segment (tasks)
+constexpr int kOverflowCap = 1 << 17;            // CTA-wide overflow LIFO (tasks)
+constexpr unsigned kTasksPerCta = (unsigned)(kLRThreads * kSeg + kOverflowCap);
+constexpr unsigned kTagNode = 3u, kTagChild = 4u, kTagZ = 5u;
+
+struct TaskArrays {
+  double* s;                    // start age of the lineage
+  double* lam;                  // lineage rate (ClaDS2 only; may be null)
+  unsigned long long* id;       // 64-bit node id (id0 | id1 << 32)
+  unsigned short* owner;        // particle slot within the CTA's batch
+  unsigned cap;                 // tasks per CTA
+};
+
+struct LRArgs {
+  PropArgs p;
+  TaskArrays t;
+  unsigned n_batches;
+};
+
+__device__ __forceinline__ uint4 side_block(unsigned long long seed, unsigned long long id,
+                                            uint32_t n, uint32_t t, uint32_t tag) {
+  return philox4x32_10(make_uint4((uint32_t)id, (uint32_t)(id >> 32), n, (tag << 28) | t),
+                       (uint32_t)seed, (uint32_t)(seed >> 32));
+}
+__device__ __forceinline__ unsigned long long root_id(unsigned k) {
+  return (unsigned long long)k | (0xFFFFFFFFull << 32);
+}
+
+// Outcome of evaluating one side-tree node.
+struct NodeOut {
+  double s2, la, lb;             // daughters' start age and rates (rates: ClaDS2)
+  unsigned long long ida, idb;   // daughters' ids
+};
+enum { NODE_LEAF = 0, NODE_DETECTED = 1, NODE_BIRTH = 2 };
+
+// Per-owner constants kept in shared memory during phase 2.
+struct OwnerCrbd { double tot, pb; };
+struct OwnerClads2 { double eps, alpha, sigma, pb; };
+
+// ---------------------------------------------------------------------------
+// CRBD under §R-18
+// ---------------------------------------------------------------------------
+struct CrbdLR {
+  typedef Crbd::State State;
+  typedef OwnerCrbd Owner;
+  static constexpr int kPlanes = Crbd::kPlanes;
+  static constexpr bool kHasLam = false;
+  __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
+    Crbd::load(s, P, st, i);
+  }
+  __device__ static void store(const State& s, uint4* P, unsigned long long st, unsigned long long i) {
+    Crbd::store(s, P, st, i);
+  }
+  __device__ static int pc(const State& s) { return s.pc; }
+
+  // Phase 1: INIT (if pc = b0) and the main-stream part of BRANCH.  Calls
+  // push(s, lam, k) for hidden event k.  Returns false if the particle is
+  // already dead (never for CRBD).
+  template <class Push>
+  __device__ static bool main_part(State& s, double& lw, Rng& r, const ModelConst& C, Owner& ow,
+                                   int& K, Push push) {
+    const double rho = C.p[0];
+    if (s.pc == 0) {
+      s.lambda = C.p[1] >= 0.0 ? C.p[1] : d_gamma(r, 1.0, 1.0);
+      s.mu = C.p[2] >= 0.0 ? C.p[2] : d_gamma(r, 1.0, 0.5);
+      s.branch = 0;
+      s.pc = 1;
+    }
+    const double* b = C.table + 3 * s.branch;
+    const double tp = __ldg(b), tc = __ldg(b + 1);
+    const bool internal = __ldg(b + 2) != 0.0;
+    lw = lw + (-s.mu * (tp - tc));
+    lw = lw + (internal ? log(s.lambda) : log(rho));
+    ow.tot = s.lambda + s.mu;           // before any push: phase-1 DFS reads them
+    ow.pb = s.lambda / ow.tot;
+    double t = tp;
+    K = 0;
+    for (;;) {
+      t = t - d_exp(r, s.lambda);
+      if (t <= tc) break;
+      push(t, 0.0, (unsigned)K);
+      ++K;
+    }
+    s.branch = s.branch + 1;
+    s.pc = (s.branch == C.n) ? kStop : 1;
+    return true;
+  }
+
+  // Phase 2: one node (lineage from its birth at age s to its next event).
+  __device__ static int node(double s, double, unsigned long long id, const Owner& ow, uint32_t n,
+                             uint32_t t, unsigned long long seed, double rho, NodeOut& out) {
+    const uint4 B = side_block(seed, id, n, t, kTagNode);
+    const double u0 = hq(B.x, B.y), u1 = hq(B.z, B.w);
+    const double d = -log(u0) / ow.tot;
+    if (d > s) return u1 < rho ? NODE_DETECTED : NODE_LEAF;
+    if (!(u1 < ow.pb)) return NODE_LEAF;                       // death
+    const uint4 Cb = side_block(seed, id, n, t, kTagChild);
+    out.s2 = s - d;
+    out.la = out.lb = 0.0;
+    out.ida = ((unsigned long long)Cb.y << 32) | Cb.x;
+    out.idb = ((unsigned long long)Cb.w << 32) | Cb.z;
+    return NODE_BIRTH;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// ClaDS2 under §R-18 (with the §R-14b rate guard)
+// ---------------------------------------------------------------------------
+struct Clads2LR {
+  typedef Clads2::State State;
+  typedef OwnerClads2 Owner;
+  static constexpr int kPlanes = Clads2::kPlanes;
+  static constexpr bool kHasLam = true;
+  __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
+    Clads2::load(s, P, st, i);
+  }
+  __device__ static void store(const State& s, uint4* P, unsigned long long st, unsigned long long i) {
+    Clads2::store(s, P, st, i);
+  }
+  __device__ static int pc(const State& s) { return s.pc; }
+
+  template <class Push>
+  __device__ static bool main_part(State& s, double& lw, Rng& r, const ModelConst& C, Owner& ow,
+                                   int& K, Push push) {
+    const double rho = C.p[0];
+    K = 0;
+    if (s.pc == 0) {                          // INIT + root split: identical to §R-14
+      Diag dg;
+      Clads2::step(s, lw, r, C, dg);
+    }
+    ow.eps = s.eps; ow.alpha = s.alpha; ow.sigma = s.sigma;
+    ow.pb = 1.0 / (1.0 + s.eps);
+    const double* b = C.table + 4 * s.branch;
+    const double tp = __ldg(b), tc = __ldg(b + 1);
+    const bool internal = __ldg(b + 2) != 0.0;
+    const bool first_left = __ldg(b + 3) != 0.0;
+    bool killed = Clads2::bad_rate(s.lam);
+    double t = tp;
+    while (!killed) {
+      const double dt = d_exp(r, s.lam);
+      if (t - dt <= tc) {
+        lw = lw + (-s.eps * s.lam * (t - tc));
+        break;
+      }
+      lw = lw + (-s.eps * s.lam * dt);
+      t = t - dt;
+      const double zs = d_normal(r, 0.0, 1.0);
+      const double zc = d_normal(r, 0.0, 1.0);
+      const double ls = Clads2::daughter(s, s.lam, zs);
+      if (Clads2::bad_rate(ls)) { killed = true; break; }
+      push(t, ls, (unsigned)K);
+      ++K;
+      s.lam = Clads2::daughter(s, s.lam, zc);
+      if (Clads2::bad_rate(s.lam)) { killed = true; break; }
+    }
+    if (!killed && internal) {
+      lw = lw + log(s.lam);
+      const double zl = d_normal(r, 0.0, 1.0);
+      const double zr = d_normal(r, 0.0, 1.0);
+      const double rl = Clads2::daughter(s, s.lam, zl), rr = Clads2::daughter(s, s.lam, zr);
+      if (Clads2::bad_rate(rl) || Clads2::bad_rate(rr)) {
+        killed = true;
+      } else {
+        Clads2::push(s, first_left ? rr : rl);
+        s.lam = first_left ? rl : rr;
+      }
+    } else if (!killed) {
+      lw = lw + log(rho);
+      if (s.branch + 1 < C.n) s.lam = Clads2::pop(s);
+    }
+    if (killed) lw = -INFINITY;
+    s.branch = s.branch + 1;
+    s.pc = (s.branch == C.n) ? kStop : 1;
+    return !killed;
+  }
+
+  __device__ static int node(double s, double lam, unsigned long long id, const Owner& ow, uint32_t n,
+                             uint32_t t, unsigned long long seed, double rho, NodeOut& out) {
+    const uint4 B = side_block(seed, id, n, t, kTagNode);
+    const double u0 = hq(B.x, B.y), u1 = hq(B.z, B.w);
+    const double d = -log(u0) / (lam * (1.0 + ow.eps));
+    if (d > s) return u1 < rho ? NODE_DETECTED : NODE_LEAF;
+    if (!(u1 < ow.pb)) return NODE_LEAF;
+    const uint4 Z = side_block(seed, id, n, t, kTagZ);
+    const double rad = sqrt(-2.0 * log(hq(Z.x, Z.y)));
+    const double th = kTwoPi * hq(Z.z, Z.w);
+    const double za = rad * cos(th), zb = rad * sin(th);
+    out.la = ow.alpha * lam * exp(ow.sigma * za);
+    out.lb = ow.alpha * lam * exp(ow.sigma * zb);
+    if (Clads2::bad_rate(out.la) || Clads2::bad_rate(out.lb)) return NODE_DETECTED;   // rate guard
+    const uint4 Cb = side_block(seed, id, n, t, kTagChild);
+    out.s2 = s - d;
+    out.ida = ((unsigned long long)Cb.y << 32) | Cb.x;
+    out.idb = ((unsigned long long)Cb.w << 32) | Cb.z;
+    return NODE_BIRTH;
+  }
+};
+
+// ---------------------------------------------------------------------------
+template <class M>
+__global__ void __launch_bounds__(kLRThreads, SMC_LR_MINB) propagate_lr_kernel(LRArgs a, ModelConst C) {
+  __shared__ int s_cnt[kLRThreads];          // tasks in owner o's segment
+  __shared__ int s_sel[kLRThreads];          // this round: lane -> task slot (owner-written)
+  __shared__ int s_ovtop;                     // overflow stack top
+  __shared__ int s_wsum[kLRThreads / 32];
+  __shared__ unsigned s_batch;
+  __shared__ int s_dead[kLRThreads];          // 0 alive, 1 detected/rejected, 2 node cap
+  __shared__ unsigned s_nodes[kLRThreads];
+  __shared__ typename M::Owner s_own[kLRThreads];
+  __shared__ int s_taskcap;
+  __shared__ long long s_key[kLRThreads / 32];
+  __shared__ unsigned long long s_acc[3][kLRThreads / 32];
+  const PropArgs& p = a.p;
+  if (*(volatile unsigned*)&p.ctrl->done) return;
+  const unsigned epoch = p.ctrl->epoch;
+  const unsigned long long seed = p.ctrl->seed;
+  const double rho = C.p[0];
+  const int tid = threadIdx.x;
+  const unsigned long long tbase = (unsigned long long)blockIdx.x * kTasksPerCta;
+  double* T_s = a.t.s + tbase;
+  double* T_lam = M::kHasLam ? a.t.lam + tbase : nullptr;
+  unsigned long long* T_id = a.t.id + tbase;
+  unsigned short* T_own = a.t.owner + tbase;
+  if (tid == 0) s_taskcap = 0;
+  // push a task for owner o: its segment, else the overflow stack
+  auto push_task = [&](int o, double s0, double lam0, unsigned long long id) {
+    int pos = atomicAdd(&s_cnt[o], 1);
+    unsigned long long slot;
+    if (pos < kSeg) {
+      slot = (unsigned long long)o * kSeg + pos;
+    } else {
+      const int q = atomicAdd(&s_ovtop, 1);
+      if (q >= kOverflowCap) { s_taskcap = 1; return; }
+      slot = (unsigned long long)kLRThreads * kSeg + q;
+    }
+    T_s[slot] = s0;
+    if (M::kHasLam) T_lam[slot] = lam0;
+    T_id[slot] = id;
+    T_own[slot] = (unsigned short)o;
+  };
+
+  long long key = LLONG_MIN;
+  unsigned long long n_end = 0, n_start = 0, drw = 0, ovf = 0, roots = 0;
+  bool bad = false;
+  unsigned max_rounds = 0, max_nodes = 0;
+
+  for (;;) {
+    if (tid == 0) {
+      s_batch = atomicAdd(&p.ctrl->batch, 1u);
+      s_ovtop = 0;
+    }
+    s_cnt[tid] = 0;
+    s_dead[tid] = 0;
+    s_nodes[tid] = 0;
+    __syncthreads();
+    const unsigned batch = s_batch;
+    if (batch >= a.n_batches) break;
+    const unsigned long long i = (unsigned long long)batch * kLRThreads + tid;
+    const bool valid = i < p.n_local;
+    const uint32_t n_glob = (uint32_t)(p.shard_base + i);
+    // ---------------- phase 1: the particle's own stream
+    typename M::State st;
+    double lw = 0.0;
+    int K = 0;
+    bool active = false;
+    if (valid) {
+      M::load(st, p.planes, p.n_local, i);
+      if (M::pc(st) != kStop) {
+        active = true;
+        ++n_start;
+        Rng r(seed, n_glob, epoch);
+        auto push = [&](double s0, double lam0, unsigned k) { push_task(tid, s0, lam0, root_id(k)); };
+        if (!M::main_part(st, lw, r, C, s_own[tid], K, push)) s_dead[tid] = 1;
+        roots += (unsigned long long)K;
+        drw += 2ull * r.blk - (r.has_spare ? 1ull : 0ull);
+      }
+    }
+    __syncthreads();
+    if (s_cnt[tid] > kSeg) s_cnt[tid] = kSeg;     // pushes beyond the segment went to overflow
+    if (tid == 0 && s_ovtop > kOverflowCap) s_ovtop = kOverflowCap;
+    // ---------------- phase 2: cooperative side-tree evaluation
+    unsigned rounds = 0;
+    const int warp_id = tid >> 5, lane_id = tid & 31;
+    for (;;) {
+      const int c = s_cnt[tid];
+      const int active = __syncthreads_count(c > 0);
+      const int ov = s_ovtop;
+      if (active == 0 && ov == 0) break;
+      const int W = active ? max(1, kLRThreads / active) : 0;
+      const int m = min(c, W);
+      // exclusive block scan of m
+      int incl = m;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane_id >= d) incl += o;
+      }
+      if (lane_id == 31) s_wsum[warp_id] = incl;
+      __syncthreads();
+      int woff = 0, T = 0;
+#pragma unroll
+      for (int w = 0; w < kLRThreads / 32; ++w) {
+        const int v = s_wsum[w];
+        woff += w < warp_id ? v : 0;
+        T += v;
+      }
+      {
+        // owner tid writes the slots of its top m tasks to lanes [off, off+m)
+        const int off = woff + incl - m;
+        const int seg = tid * kSeg;
+        for (int j = 0; j < m; ++j) s_sel[off + j] = seg + (c - 1 - j);
+      }
+      __syncthreads();
+      // lane -> task
+      bool have = false;
+      double ts = 0.0, tl = 0.0;
+      unsigned long long tidv = 0;
+      int o = 0;
+      unsigned long long slot = 0;
+      if (tid < T) {
+        slot = (unsigned long long)s_sel[tid];
+        have = true;
+      } else if (tid - T < ov) {
+        slot = (unsigned long long)kLRThreads * kSeg + (ov - 1 - (tid - T));
+        have = true;
+      }
+      if (have) {
+        ts = T_s[slot];
+        if (M::kHasLam) tl = T_lam[slot];
+        tidv = T_id[slot];
+        o = T_own[slot];
+      }
+      __syncthreads();
+      s_cnt[tid] = c - m;
+      if (tid == 0) s_ovtop = ov - min(ov, kLRThreads - T);
+      __syncthreads();
+      if (have && s_dead[o] == 0) {
+        const unsigned cnt = atomicAdd(&s_nodes[o], 1u) + 1u;
+        if (cnt > kSideNodeCap) {
+          s_dead[o] = 2;
+        } else {
+          const uint32_t n_owner = (uint32_t)(p.shard_base + (unsigned long long)batch * kLRThreads + o);
+          drw += 2;
+          NodeOut out;
+          const int res = M::node(ts, tl, tidv, s_own[o], n_owner, epoch, seed, rho, out);
+          if (res == NODE_DETECTED) {
+            if (s_dead[o] == 0) s_dead[o] = 1;
+          } else if (res == NODE_BIRTH) {
+            push_task(o, out.s2, out.lb, out.idb);
+            push_task(o, out.s2, out.la, out.ida);     // first daughter on top (DFS order)
+          }
+        }
+      }
+      __syncthreads();
+      if (s_cnt[tid] > kSeg) s_cnt[tid] = kSeg;
+      if (tid == 0 && s_ovtop > kOverflowCap) s_ovtop = kOverflowCap;
+      ++rounds;
+    }
+    max_rounds = rounds > max_rounds ? rounds : max_rounds;
+    max_nodes = s_nodes[tid] > max_nodes ? s_nodes[tid] : max_nodes;
+    // ---------------- phase 3: finish the particle
+    if (valid) {
+      if (active) {
+        const int dead = s_dead[tid];
+        if (dead) {
+          lw = -INFINITY;
+          if (dead == 2) ++ovf;
+        } else {
+          for (int k = 0; k < K; ++k) lw = lw + kLn2;
+        }
+        M::store(st, p.planes, p.n_local, i);
+        if (dead == 2) atomicMin(&p.ctrl->first_err, (unsigned long long)n_glob);
+      }
+      p.lw[i] = lw;
+      if (M::pc(st) != kStop) ++n_end;
+      const bool b = isnan(lw) || lw == INFINITY;
+      bad |= b;
+      const long long k = order_key(lw);
+      key = k > key ? k : key;
+    }
+    __syncthreads();
+  }
+  // ---------------- epilogue: one set of atomics per CTA
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const long long o = __shfl_xor_sync(0xffffffffu, key, d);
+    key = o > key ? o : key;
+    n_end += __shfl_xor_sync(0xffffffffu, n_end, d);
+    n_start += __shfl_xor_sync(0xffffffffu, n_start, d);
+    drw += __shfl_xor_sync(0xffffffffu, drw, d);
+    ovf += __shfl_xor_sync(0xffffffffu, ovf, d);
+  }
+  const int warp = tid >> 5, lane = tid & 31;
+  if (lane == 0) {
+    s_key[warp] = key;
+    s_acc[0][warp] = n_end;
+    s_acc[1][warp] = n_start;
+    s_acc[2][warp] = drw;
+  }
+  const int any_bad = __syncthreads_or(bad);
+  const int any_ovf = __syncthreads_or(ovf != 0);
+  unsigned long long ovf_sum = ovf;
+  (void)ovf_sum;
+  if (tid == 0) {
+    long long k = s_key[0];
+    unsigned long long e = 0, st = 0, dr = 0;
+    for (int w = 0; w < kLRThreads / 32; ++w) {
+      k = s_key[w] > k ? s_key[w] : k;
+      e += s_acc[0][w];
+      st += s_acc[1][w];
+      dr += s_acc[2][w];
+    }
+    RecA* rec = p.recA + (epoch & 1) * p.world + p.rank;
+    atomicMax(&rec->key, k);
+    if (e) atomicAdd(&rec->alive, (unsigned)e);
+    if (any_bad) atomicOr(&rec->flags, 1u);
+    if (s_taskcap) atomicOr(&rec->flags, 2u);
+    if (st) atomicAdd(&p.ctrl->alive_steps, st);
+    if (dr) atomicAdd(&p.ctrl->draws, dr);
+  }
+  if (any_ovf && lane == 0 && ovf) atomicAdd(&p.ctrl->overflow, ovf);
+  // diagnostics (one atomic per warp)
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    roots += __shfl_xor_sync(0xffffffffu, roots, d);
+    max_nodes = max(max_nodes, __shfl_xor_sync(0xffffffffu, max_nodes, d));
+  }
+  if (lane == 0) {
+    if (roots) atomicAdd(&p.ctrl->side_roots, roots);
+    atomicMax(&p.ctrl->max_side_nodes, max_nodes);
+    if (tid == 0) atomicMax(&p.ctrl->max_rounds, max_rounds);
+  }
+}
+
+}  // namespace smc

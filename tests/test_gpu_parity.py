@@ -22,10 +22,16 @@ pytestmark = pytest.mark.gpu
 RTOL = 1e-9
 
 
+TREE_KINDS = (oracle.CRBD, oracle.CLADS2, oracle.CRBD_LR, oracle.CLADS2_LR)
+LINEAGE = {oracle.CRBD_LR: oracle.CRBD, oracle.CLADS2_LR: oracle.CLADS2}
+
+
 def both(smc, kind, tree_or_data, params, N, seed, shards=1):
-    """(gpu Smc, oracle Smc) for the same model/N/seed, not yet run."""
-    if kind in (oracle.CRBD, oracle.CLADS2):
-        gm = smc.Model(kind, smc.tree_data(tree_or_data), params)
+    """(gpu Smc, oracle Smc) for the same model/N/seed, not yet run.  The
+    oracle's lineage-keyed kinds map to the GPU kind + SMC_FLAG_LINEAGE_RNG."""
+    if kind in TREE_KINDS:
+        flags = smc.FLAG_LINEAGE_RNG if kind in LINEAGE else 0
+        gm = smc.Model(LINEAGE.get(kind, kind), smc.tree_data(tree_or_data), params, flags=flags)
         od = oracle.tree_blob(tree_or_data)
     else:
         gm = smc.Model(kind, tree_or_data, params)
@@ -143,25 +149,40 @@ def test_ssm(smc):
     run_pair(smc, oracle.SSM, inputs.ssm_series(50), inputs.SSM_PARAMS, 3000, 5)
 
 
+CRBD_K = pytest.mark.parametrize("ck", [oracle.CRBD, oracle.CRBD_LR], ids=["seq", "lineage"])
+CLADS_K = pytest.mark.parametrize("ck", [oracle.CLADS2, oracle.CLADS2_LR], ids=["seq", "lineage"])
+
+
+@CRBD_K
 @pytest.mark.parametrize("N,seed", [(1000, 1), (2049, 2)])
-def test_crbd_tree5(smc, N, seed):
-    run_pair(smc, oracle.CRBD, inputs.tree("tree5"), inputs.CRBD_PARAMS, N, seed)
+def test_crbd_tree5(smc, ck, N, seed):
+    run_pair(smc, ck, inputs.tree("tree5"), inputs.CRBD_PARAMS, N, seed)
 
 
-def test_crbd_tree5_fixed_rates(smc):
-    run_pair(smc, oracle.CRBD, inputs.tree("tree5"), [1.0, 0.3, 0.1], 1500, 4)
+@CRBD_K
+@pytest.mark.parametrize("prm", [[1.0, 0.3, 0.1], [0.5, 0.3, 0.1], [1.0, 0.5, 0.0]])
+def test_crbd_tree5_fixed_rates(smc, ck, prm):
+    run_pair(smc, ck, inputs.tree("tree5"), prm, 1500, 4)
 
 
-def test_crbd_tree90(smc):
-    run_pair(smc, oracle.CRBD, inputs.tree("tree90"), inputs.CRBD_PARAMS, 3000, 90, per_epoch=False)
+@CRBD_K
+def test_crbd_tree90(smc, ck):
+    run_pair(smc, ck, inputs.tree("tree90"), inputs.CRBD_PARAMS, 3000, 90, per_epoch=False)
 
 
-def test_clads2_tree5(smc):
-    run_pair(smc, oracle.CLADS2, inputs.tree("tree5"), inputs.CLADS2_PARAMS, 2000, 6)
+@CRBD_K
+def test_crbd_tree90_per_epoch_prefix(smc, ck):
+    run_pair(smc, ck, inputs.tree("tree90"), inputs.CRBD_PARAMS, 20_000, 91, max_epochs=12)
 
 
-def test_clads2_tree90(smc):
-    run_pair(smc, oracle.CLADS2, inputs.tree("tree90"), inputs.CLADS2_PARAMS, 2000, 7, per_epoch=False)
+@CLADS_K
+def test_clads2_tree5(smc, ck):
+    run_pair(smc, ck, inputs.tree("tree5"), inputs.CLADS2_PARAMS, 2000, 6)
+
+
+@CLADS_K
+def test_clads2_tree90(smc, ck):
+    run_pair(smc, ck, inputs.tree("tree90"), inputs.CLADS2_PARAMS, 2000, 7, per_epoch=False)
 
 
 def test_seir(smc):
@@ -198,16 +219,25 @@ def test_virtual_shards_vs_oracle(smc):
     run_pair(smc, oracle.CLADS2, inputs.tree("tree5"), inputs.CLADS2_PARAMS, 3 * 1001, 12, shards=3)
 
 
+@pytest.mark.parametrize("shards", [2, 4])
+def test_virtual_shards_lineage(smc, shards):
+    run_pair(smc, oracle.CRBD_LR, inputs.tree("tree90"), inputs.CRBD_PARAMS, shards * 2500, 13,
+             shards=shards, per_epoch=False)
+
+
 # ------------------------------------------------------------- full size
-def test_crbd_full_size_prefix(smc):
+@CRBD_K
+def test_crbd_full_size_prefix(smc, ck):
     """BASELINE configs[1] at 10^6 particles, first 4 epochs, element by element."""
-    run_pair(smc, oracle.CRBD, inputs.tree("tree90"), inputs.CRBD_PARAMS, 1_000_000, 1,
+    run_pair(smc, ck, inputs.tree("tree90"), inputs.CRBD_PARAMS, 1_000_000, 1,
              per_epoch=True, max_epochs=4)
 
 
 # ------------------------------------------------------------- whole-run CUDA graph
 @pytest.mark.parametrize("kind,data,params,N", [
     (oracle.CRBD, "tree90", inputs.CRBD_PARAMS, 5000),
+    (oracle.CRBD_LR, "tree90", inputs.CRBD_PARAMS, 5000),
+    (oracle.CLADS2_LR, "tree90", inputs.CLADS2_PARAMS, 3000),
     (oracle.GEOMETRIC, None, inputs.GEOMETRIC_PARAMS, 3001),     # particles stop at different epochs
     (oracle.SEIR, "seir", None, 1500),
     (oracle.CONSTW, None, inputs.CONSTW_PARAMS, 10),

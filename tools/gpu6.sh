@@ -1,0 +1,7 @@
+timeout 300 python bench.py --steps 5 --warmup 3 --cpu-budget 10 2>&1 | tail -1
+timeout 300 python bench.py --steps 3 --warmup 3 --rng sequential --no-cpu-baseline --no-e2e 2>&1 | tail -1
+timeout 600 python bench.py --workload clads2 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_crbd_lr.csv python tools/profile_run.py --workload crbd --sweeps 1 > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_clads2_lr.csv python tools/profile_run.py --workload clads2 --sweeps 1 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:propagate_lr -s 60 -c 1 -o gpurun_out/prof_prop_lr python tools/profile_run.py --workload crbd > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:propagate_lr -s 3 -c 1 -o gpurun_out/prof_prop_lr_e3 python tools/profile_run.py --workload crbd > /dev/null 2>&1

@@ -15,6 +15,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="crbd")
 ap.add_argument("--n", type=int, default=1_000_000)
 ap.add_argument("--sweeps", type=int, default=1)
+ap.add_argument("--rng", default="lineage")
 args = ap.parse_args()
 if args.workload == "resample":
     n = args.n
@@ -28,10 +29,12 @@ if args.workload == "resample":
         r.device(lw, st, out, anc, epoch=e)
     torch.cuda.synchronize()
 else:
-    m = {"crbd": lambda: smc.Model.crbd(inputs.tree("tree90")),
-         "clads2": lambda: smc.Model.clads2(inputs.tree("tree90")),
+    lin = args.rng == "lineage"
+    m = {"crbd": lambda: smc.Model.crbd(inputs.tree("tree90"), lineage=lin),
+         "clads2": lambda: smc.Model.clads2(inputs.tree("tree90"), lineage=lin),
          "seir": lambda: smc.Model.seir(inputs.seir_series())}[args.workload]()
     h = smc.Smc(m, args.n, 1)
+    h.set_graph(False)     # ncu does not profile kernels inside conditional-graph bodies
     for s in range(args.sweeps):
         h.reset(1 + s)
         h.run()
