@@ -234,6 +234,16 @@ int smc_resample_host(smc_handle h, const double* lw, const void* state_in, void
  * algorithmic-bytes count); synchronises. */
 int smc_last_distinct(smc_handle h, uint64_t* out);
 
+/* Host-side planner of the global systematic grid (no device needed): given
+ * the all-gathered integer shard totals W_g (w_lohi[2g] = low 64 bits, [2g+1]
+ * = high), world shards of n_per particles and the resampling integer z
+ * (u = (2z+1) 2^-54), writes out[0..world] with out[g] = #{grid points j :
+ * (j + u) W < N P_g}, P_g = W_0 + ... + W_{g-1}: shard g's particles fill the
+ * global output slots [out[g], out[g+1]).  Identical integer arithmetic to the
+ * device kernels; used for migration accounting and by the CPU tests. */
+int smc_plan_ranges(const uint64_t* w_lohi, int32_t world, uint64_t n_per, uint64_t z,
+                    uint64_t* out);
+
 /* Symbols-only helper: ABI version of the loaded library. */
 int smc_abi_version(void);
 

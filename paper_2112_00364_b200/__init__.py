@@ -96,6 +96,8 @@ _sig = {
     "smc_resample_host": ([H, C.POINTER(C.c_double), C.c_void_p, C.c_void_p,
                            C.POINTER(C.c_uint32), C.c_uint32, C.POINTER(C.c_double)], C.c_int),
     "smc_last_distinct": ([H, C.POINTER(C.c_uint64)], C.c_int),
+    "smc_plan_ranges": ([C.POINTER(C.c_uint64), C.c_int32, C.c_uint64, C.c_uint64,
+                         C.POINTER(C.c_uint64)], C.c_int),
 }
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_lib, _name)
@@ -318,6 +320,20 @@ class Resampler:
         v = C.c_uint64(0)
         _check(self.h, _lib.smc_last_distinct(self.h, C.byref(v)))
         return v.value
+
+
+def plan_ranges(shard_totals, n_per: int, z: int):
+    """Output slot range of each shard for integer shard totals (Python ints)
+    and resampling integer z: returns out[0..world] (C++ planner, host only)."""
+    world = len(shard_totals)
+    w = np.zeros(2 * world, dtype=np.uint64)
+    for g, W in enumerate(shard_totals):
+        w[2 * g] = W & (2 ** 64 - 1)
+        w[2 * g + 1] = W >> 64
+    out = np.zeros(world + 1, dtype=np.uint64)
+    _check(None, _lib.smc_plan_ranges(w.ctypes.data_as(C.POINTER(C.c_uint64)), world, int(n_per),
+                                      int(z), out.ctypes.data_as(C.POINTER(C.c_uint64))))
+    return [int(v) for v in out]
 
 
 def aos_to_soa(states: np.ndarray) -> np.ndarray:

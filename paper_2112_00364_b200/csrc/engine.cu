@@ -1046,6 +1046,53 @@ int smc_resample_host(smc_handle h, const double* lw, const void* state_in, void
   return SMC_OK;
 }
 
+// Host-side exact planner (same integer arithmetic as Grid::count_below).
+static bool plan_below(unsigned long long j, u128 C, u128 W, unsigned long long z2p1, u128 Nsc) {
+  // (j 2^54 + 2z + 1) W < N 2^54 C  in 256-bit
+  auto mul = [](u128 a, u128 b, unsigned long long r[4]) {
+    const unsigned long long a0 = (unsigned long long)a, a1 = (unsigned long long)(a >> 64);
+    const unsigned long long b0 = (unsigned long long)b, b1 = (unsigned long long)(b >> 64);
+    const u128 p00 = (u128)a0 * b0, p01 = (u128)a0 * b1, p10 = (u128)a1 * b0, p11 = (u128)a1 * b1;
+    r[0] = (unsigned long long)p00;
+    u128 mid = (p00 >> 64) + (unsigned long long)p01 + (unsigned long long)p10;
+    r[1] = (unsigned long long)mid;
+    u128 hi = (mid >> 64) + (p01 >> 64) + (p10 >> 64) + (unsigned long long)p11;
+    r[2] = (unsigned long long)hi;
+    r[3] = (unsigned long long)(hi >> 64) + (unsigned long long)(p11 >> 64);
+  };
+  unsigned long long l[4], r[4];
+  mul(((u128)j << 54) + z2p1, W, l);
+  mul(Nsc, C, r);
+  for (int i = 3; i >= 0; --i)
+    if (l[i] != r[i]) return l[i] < r[i];
+  return false;
+}
+static unsigned long long plan_count(u128 C, u128 W, unsigned long long z2p1, unsigned long long N) {
+  const u128 Nsc = (u128)N << 54;
+  unsigned long long lo = 0, hi = N;          // smallest j in [0, N] with !below(j)
+  while (lo < hi) {
+    const unsigned long long mid = lo + (hi - lo) / 2;
+    if (plan_below(mid, C, W, z2p1, Nsc)) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+int smc_plan_ranges(const uint64_t* w_lohi, int32_t world, uint64_t n_per, uint64_t z,
+                    uint64_t* out) {
+  if (!w_lohi || !out || world < 1 || n_per == 0 || z >= (1ull << 53))
+    return fail(nullptr, SMC_EINVAL, "bad planner arguments");
+  const unsigned long long N = n_per * (unsigned long long)world;
+  u128 W = 0;
+  for (int g = 0; g < world; ++g) W += ((u128)w_lohi[2 * g + 1] << 64) | w_lohi[2 * g];
+  if (W == 0) return fail(nullptr, SMC_EREJECTED, "total weight is zero");
+  u128 P = 0;
+  for (int g = 0; g <= world; ++g) {
+    out[g] = plan_count(P, W, 2 * z + 1, N);
+    if (g < world) P += ((u128)w_lohi[2 * g + 1] << 64) | w_lohi[2 * g];
+  }
+  return SMC_OK;
+}
+
 int smc_last_distinct(smc_handle h, uint64_t* out) {
   if (!h || !out) return fail(h, SMC_EINVAL, "NULL argument");
   CU(cudaStreamSynchronize(h->stream));

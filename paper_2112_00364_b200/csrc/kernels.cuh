@@ -472,6 +472,7 @@ __global__ void __launch_bounds__(kThreads) anc_gather_kernel(ResArgs a) {
     }
     a.dst_anc[dshard][dl] = (uint32_t)(a.shard_base + src);
   }
+  if (a.world > 1) __threadfence_system();   // peer stores visible before the epoch barrier
 }
 
 // ============================================================================

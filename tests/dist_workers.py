@@ -1,0 +1,69 @@
+"""Worker functions for the multi-process tests (importable by spawn)."""
+import ctypes as C
+import os
+import socket
+
+import numpy as np
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def init(rank, world, port, backend="gloo"):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group(backend, rank=rank, world_size=world)
+    return dist
+
+
+def cpu_worker(rank, world, port, outdir):
+    """Host logic of the sharded path over gloo (no GPU needed)."""
+    dist = init(rank, world, port)
+    import paper_2112_00364_b200 as smc
+    from paper_2112_00364_b200 import dist as sdist
+    rng = np.random.default_rng(1000 + rank)
+    # 1. each rank contributes its shard total; every rank plans the same ranges
+    my_total = int(rng.integers(0, 2 ** 62)) * int(rng.integers(1, 2 ** 30))
+    totals = [int(x) for x in (v for v in
+              (int.from_bytes(b, "little") for b in sdist.allgather_bytes(my_total.to_bytes(16, "little"))))]
+    z = 0x1234567890ABC
+    plan = smc.plan_ranges(totals, 1000, z)
+    # 2. the host all-gather callback used by the C library
+    ag = sdist.HostAllgather()
+    send = (C.c_char * 16)(*bytes([rank + 1] * 16))
+    recv = (C.c_char * (16 * world))()
+    rc = ag.cfunc(C.cast(send, C.c_void_p), C.cast(recv, C.c_void_p), 16, None)
+    # 3. NCCL unique-id broadcast (rank 0 creates it) if NCCL loads here
+    try:
+        nid = sdist.nccl_unique_id()
+    except Exception as e:           # NCCL not loadable on this host
+        nid = repr(e).encode()
+    np.save(os.path.join(outdir, f"r{rank}.npy"),
+            np.array([totals, plan, list(bytes(recv)), rc, nid], dtype=object), allow_pickle=True)
+    dist.destroy_process_group()
+
+
+def gpu_worker(rank, world, port, outdir, n_per, seed, lineage):
+    """Real sharded path: one process per shard on the same GPU, host comm
+    (gloo) for the 16-byte records, CUDA IPC for particle migration."""
+    dist = init(rank, world, port)
+    import torch
+    torch.cuda.set_device(0)
+    import inputs
+    import paper_2112_00364_b200 as smc
+    from paper_2112_00364_b200 import dist as sdist
+    m = smc.Model.crbd(inputs.tree("tree90"), lineage=lineage)
+    h = sdist.ShardedSmc(m, n_per, seed, comm="host")
+    rc = h.run_status()
+    np.save(os.path.join(outdir, f"g{rank}.npy"),
+            np.array([rc, h.log_z, h.ancestors(), h.log_weights(), h.fields(), h.stats()], dtype=object),
+            allow_pickle=True)
+    h.close()
+    dist.barrier()
+    dist.destroy_process_group()
