@@ -106,6 +106,18 @@ __device__ __forceinline__ double d_beta(Rng& r, double a, double b) {
   return x / (x + y);
 }
 
+// lgamma(k + 1) for integer k: table lookup when the model supplies one
+// (host-computed log-factorials, identical to the host libm values), else the
+// device lgamma.  Every lgamma in the binomial code has an integer argument.
+struct LogFact {
+  const double* tbl;
+  long long n;
+  __device__ __forceinline__ double operator()(double x1) const {   // x1 = k + 1
+    const long long k = (long long)x1 - 1;
+    return (tbl && k >= 0 && k < n) ? __ldg(tbl + k) : lgamma(x1);
+  }
+};
+
 // Binomial: inversion (BINV) for n p < 10; BTRS (Hormann 1993) otherwise.
 // The BTRS normaliser h = lgamma(m+1) + lgamma(n-m+1) is only needed when
 // the squeeze fails, so it is computed lazily (same value, fewer lgammas).
@@ -123,7 +135,7 @@ __device__ long long d_binomial_inv(Rng& r, long long n, double p) {
   }
   return x;
 }
-__device__ long long d_binomial_btrs(Rng& r, long long n, double p) {
+__device__ long long d_binomial_btrs(Rng& r, long long n, double p, const LogFact& lf) {
   const double q = 1.0 - p;
   const double nd = (double)n;
   const double spq = sqrt(nd * p * q);
@@ -144,24 +156,26 @@ __device__ long long d_binomial_btrs(Rng& r, long long n, double p) {
     if (!have_h) {
       alpha = (2.83 + 5.1 / b) * spq;
       lpq = log(p / q);
-      h = lgamma(m + 1.0) + lgamma(nd - m + 1.0);
+      h = lf(m + 1.0) + lf(nd - m + 1.0);
       have_h = true;
     }
     const double lv = log(V * alpha / (a / (us * us) + b));
-    const double rhs = h - lgamma(kd + 1.0) - lgamma(nd - kd + 1.0) + (kd - m) * lpq;
+    const double rhs = h - lf(kd + 1.0) - lf(nd - kd + 1.0) + (kd - m) * lpq;
     if (lv <= rhs) return (long long)kd;
   }
 }
-__device__ __forceinline__ long long d_binomial(Rng& r, long long n, double p) {
+__device__ __forceinline__ long long d_binomial(Rng& r, long long n, double p,
+                                                const LogFact& lf = LogFact{nullptr, 0}) {
   bool flip = false;
   if (p > 0.5) { p = 1.0 - p; flip = true; }
-  const long long k = ((double)n * p < 10.0) ? d_binomial_inv(r, n, p) : d_binomial_btrs(r, n, p);
+  const long long k = ((double)n * p < 10.0) ? d_binomial_inv(r, n, p) : d_binomial_btrs(r, n, p, lf);
   return flip ? n - k : k;
 }
 
-__device__ __forceinline__ double d_binomial_logpmf(long long k, long long n, double p) {
+__device__ __forceinline__ double d_binomial_logpmf(long long k, long long n, double p,
+                                                    const LogFact& lf = LogFact{nullptr, 0}) {
   if (k < 0 || k > n) return -INFINITY;
-  double v = lgamma((double)n + 1.0) - lgamma((double)k + 1.0) - lgamma((double)(n - k) + 1.0);
+  double v = lf((double)n + 1.0) - lf((double)k + 1.0) - lf((double)(n - k) + 1.0);
   if (k > 0) v = v + (double)k * log(p);
   if (n - k > 0) v = v + (double)(n - k) * log1p(-p);
   return v;

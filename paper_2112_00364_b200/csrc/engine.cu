@@ -95,6 +95,7 @@ struct smc_ctx {
   ModelConst mc{};
   double* d_table = nullptr;
   std::vector<double> h_table;
+  double* d_logfact = nullptr;    // SEIR: lgamma(k+1) table (model setup, host libm)
   RecA* d_recA = nullptr;         // [2][world]
   u128* d_recB = nullptr;         // [2][world]
   int* d_barrier = nullptr;
@@ -393,6 +394,19 @@ int common_init(smc_ctx* h, const smc_model* m, unsigned long long n_per, int wo
   }
   h->mc.table = h->d_table;
   h->mc.flags = (int)h->flags;
+  h->mc.logfact = nullptr;
+  h->mc.n_logfact = 0;
+  if (h->kind == SMC_SEIR) {
+    // log-factorials for every integer the binomial code can see (populations
+    // up to 2^18; larger arguments fall back to the device lgamma)
+    const long long nlf = 1 << 18;
+    std::vector<double> lf(nlf);
+    for (long long k = 0; k < nlf; ++k) lf[k] = std::lgamma((double)k + 1.0);
+    CU(cudaMalloc(&h->d_logfact, nlf * sizeof(double)));
+    CU(cudaMemcpy(h->d_logfact, lf.data(), nlf * sizeof(double), cudaMemcpyHostToDevice));
+    h->mc.logfact = h->d_logfact;
+    h->mc.n_logfact = nlf;
+  }
   CU(cudaMalloc(&h->d_recA, 2 * world * sizeof(RecA)));
   CU(cudaMalloc(&h->d_recB, 2 * world * sizeof(u128)));
   CU(cudaMalloc(&h->d_barrier, sizeof(int)));
@@ -810,7 +824,7 @@ void smc_destroy(smc_handle h) {
     cudaFree(s.ipc_block); cudaFree(s.lw); cudaFree(s.tile_sum); cudaFree(s.tile_excl);
     cudaFree(s.ctrl); cudaFree(s.d_dst_planes[0]); cudaFree(s.d_dst_planes[1]); cudaFree(s.d_dst_anc);
   }
-  cudaFree(h->d_table); cudaFree(h->d_recA); cudaFree(h->d_recB); cudaFree(h->d_barrier);
+  cudaFree(h->d_table); cudaFree(h->d_logfact); cudaFree(h->d_recA); cudaFree(h->d_recB); cudaFree(h->d_barrier);
   cudaFree(h->tasks.s); cudaFree(h->tasks.lam); cudaFree(h->tasks.id); cudaFree(h->tasks.owner);
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
   if (h->graph) cudaGraphDestroy(h->graph);

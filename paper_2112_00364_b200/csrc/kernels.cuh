@@ -165,8 +165,11 @@ struct PropArgs {
   Ctrl* ctrl;
 };
 
+// Register cap per model (M::kMinBlocks resident CTAs per SM): measured on
+// B200 — CRBD 4 (64 regs, no spills), SEIR 2 (its binomial code spills below
+// 128 registers).
 template <class M>
-__global__ void __launch_bounds__(kThreads) propagate_kernel(PropArgs a, ModelConst C) {
+__global__ void __launch_bounds__(kThreads, M::kMinBlocks) propagate_kernel(PropArgs a, ModelConst C) {
   __shared__ long long s_key[kThreads / 32];
   __shared__ unsigned long long s_ovf[kThreads / 32];
   __shared__ unsigned long long s_drw[kThreads / 32];

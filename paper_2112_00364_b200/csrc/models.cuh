@@ -23,6 +23,8 @@ struct ModelConst {
   int n;                 // number of branches / series length
   int flags;
   double p[12];          // parameters
+  const double* logfact; // SEIR: lgamma(k+1), k < n_logfact (host libm values)
+  long long n_logfact;
 };
 
 // Per-thread diagnostics sink.
@@ -57,6 +59,7 @@ __device__ __forceinline__ double hi_d(uint4 v) {
 // ============================================================================
 struct Crbd {
   static constexpr int kPlanes = 2;
+  static constexpr int kMinBlocks = 4;
   struct State { double lambda, mu; int pc, branch; };
   __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
     const uint4 a = ldp(P, st, 0, i), b = ldp(P, st, 1, i);
@@ -140,6 +143,7 @@ struct Crbd {
 // ("kill": branch index and pc advance, nothing else).
 struct Clads2 {
   static constexpr int kPlanes = 6;
+  static constexpr int kMinBlocks = 2;
   static constexpr int kPend = 6;
   static constexpr double kMaxRate = 1e4;
   __device__ static bool bad_rate(double r) { return !(r <= kMaxRate); }
@@ -287,6 +291,7 @@ struct Clads2 {
 // ============================================================================
 struct Seir {
   static constexpr int kPlanes = 6;
+  static constexpr int kMinBlocks = 2;
   struct State { double lam_h, del_h, gam_h, lam_m, del_m, rho; int sh, eh, ih, rh, sm, em, im, t, pc; };
   __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
     uint4 v = ldp(P, st, 0, i); s.lam_h = lo_d(v); s.del_h = hi_d(v);
@@ -326,31 +331,32 @@ struct Seir {
       s.pc = 1;
       return false;
     }
+    const LogFact lf{C.logfact, C.n_logfact};
     const double nh = (double)nh_i;                      // DAY
     const double ph = 1.0 - exp(-(double)s.im / nh);
     const double pm = 1.0 - exp(-(double)s.ih / nh);
-    const long long tau_h = d_binomial(r, s.sh, ph);
-    const long long de_h = d_binomial(r, tau_h, s.lam_h);
-    const long long di_h = d_binomial(r, s.eh, s.del_h);
-    const long long dr_h = d_binomial(r, s.ih, s.gam_h);
+    const long long tau_h = d_binomial(r, s.sh, ph, lf);
+    const long long de_h = d_binomial(r, tau_h, s.lam_h, lf);
+    const long long di_h = d_binomial(r, s.eh, s.del_h, lf);
+    const long long dr_h = d_binomial(r, s.ih, s.gam_h, lf);
     s.sh = (int)(s.sh - de_h);
     s.eh = (int)(s.eh + de_h - di_h);
     s.ih = (int)(s.ih + di_h - dr_h);
     s.rh = (int)(s.rh + dr_h);
-    const long long tau_m = d_binomial(r, s.sm, pm);
-    const long long de_m = d_binomial(r, tau_m, s.lam_m);
-    const long long di_m = d_binomial(r, s.em, s.del_m);
+    const long long tau_m = d_binomial(r, s.sm, pm, lf);
+    const long long de_m = d_binomial(r, tau_m, s.lam_m, lf);
+    const long long di_m = d_binomial(r, s.em, s.del_m, lf);
     const long long nm = (long long)s.sm + s.em + s.im;
     const double nu_m = 1.0 / 7.0, mu_m = 6.0 / 7.0;
-    const long long births = d_binomial(r, nm, nu_m);
-    const long long s2 = d_binomial(r, s.sm - de_m, mu_m);
-    const long long e2 = d_binomial(r, s.em + de_m - di_m, mu_m);
-    const long long i2 = d_binomial(r, s.im + di_m, mu_m);
+    const long long births = d_binomial(r, nm, nu_m, lf);
+    const long long s2 = d_binomial(r, s.sm - de_m, mu_m, lf);
+    const long long e2 = d_binomial(r, s.em + de_m - di_m, mu_m, lf);
+    const long long i2 = d_binomial(r, s.im + di_m, mu_m, lf);
     s.sm = (int)(s2 + births);
     s.em = (int)e2;
     s.im = (int)i2;
     const long long y = (long long)__ldg(C.table + s.t);
-    lw = lw + d_binomial_logpmf(y, di_h, s.rho);
+    lw = lw + d_binomial_logpmf(y, di_h, s.rho, lf);
     s.t = s.t + 1;
     s.pc = (s.t == C.n) ? kStop : 1;
     return true;
@@ -362,6 +368,7 @@ struct Seir {
 // ============================================================================
 struct Geometric {
   static constexpr int kPlanes = 1;
+  static constexpr int kMinBlocks = 4;
   struct State { int pc, n; };
   __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
     const uint4 v = ldp(P, st, 0, i); s.pc = (int)v.x; s.n = (int)v.y;
@@ -385,6 +392,7 @@ struct Geometric {
 // ============================================================================
 struct Ssm {
   static constexpr int kPlanes = 1;
+  static constexpr int kMinBlocks = 4;
   struct State { double x; int pc, t; };
   __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
     const uint4 v = ldp(P, st, 0, i); s.x = lo_d(v); s.pc = (int)v.z; s.t = (int)v.w;
@@ -414,6 +422,7 @@ struct Ssm {
 // ============================================================================
 struct Constw {
   static constexpr int kPlanes = 1;
+  static constexpr int kMinBlocks = 4;
   struct State { int pc, k; };
   __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
     const uint4 v = ldp(P, st, 0, i); s.pc = (int)v.x; s.k = (int)v.y;
