@@ -74,7 +74,7 @@ __device__ __forceinline__ double d_normal(Rng& r, double mu, double sigma) {
   const double c = cos(kTwoPi * u2);
   return mu + sigma * (rad * c);
 }
-__device__ double d_gamma_mt(Rng& r, double k, double theta) {   // k > 1, Marsaglia-Tsang
+__device__ __noinline__ double d_gamma_mt(Rng& r, double k, double theta) {   // k > 1, Marsaglia-Tsang
   const double d = k - 1.0 / 3.0;
   const double c = 1.0 / sqrt(9.0 * d);
   for (;;) {
@@ -121,7 +121,7 @@ struct LogFact {
 // Binomial: inversion (BINV) for n p < 10; BTRS (Hormann 1993) otherwise.
 // The BTRS normaliser h = lgamma(m+1) + lgamma(n-m+1) is only needed when
 // the squeeze fails, so it is computed lazily (same value, fewer lgammas).
-__device__ long long d_binomial_inv(Rng& r, long long n, double p) {
+__device__ __noinline__ long long d_binomial_inv(Rng& r, long long n, double p) {
   const double q = 1.0 - p;
   const double sr = p / q;
   const double a = (double)(n + 1) * sr;
@@ -135,7 +135,7 @@ __device__ long long d_binomial_inv(Rng& r, long long n, double p) {
   }
   return x;
 }
-__device__ long long d_binomial_btrs(Rng& r, long long n, double p, const LogFact& lf) {
+__device__ __noinline__ long long d_binomial_btrs(Rng& r, long long n, double p, const LogFact& lf) {
   const double q = 1.0 - p;
   const double nd = (double)n;
   const double spq = sqrt(nd * p * q);
@@ -164,15 +164,18 @@ __device__ long long d_binomial_btrs(Rng& r, long long n, double p, const LogFac
     if (lv <= rhs) return (long long)kd;
   }
 }
-__device__ __forceinline__ long long d_binomial(Rng& r, long long n, double p,
-                                                const LogFact& lf = LogFact{nullptr, 0}) {
+// Out of line on purpose: SEIR calls it 11 times per day; inlining every copy
+// of BTRS + inversion made the kernel thrash the instruction cache (ncu:
+// "no_instruction" stalls 30 cycles per issue).
+__device__ __noinline__ long long d_binomial(Rng& r, long long n, double p,
+                                            const LogFact& lf = LogFact{nullptr, 0}) {
   bool flip = false;
   if (p > 0.5) { p = 1.0 - p; flip = true; }
   const long long k = ((double)n * p < 10.0) ? d_binomial_inv(r, n, p) : d_binomial_btrs(r, n, p, lf);
   return flip ? n - k : k;
 }
 
-__device__ __forceinline__ double d_binomial_logpmf(long long k, long long n, double p,
+__device__ __noinline__ double d_binomial_logpmf(long long k, long long n, double p,
                                                     const LogFact& lf = LogFact{nullptr, 0}) {
   if (k < 0 || k > n) return -INFINITY;
   double v = lf((double)n + 1.0) - lf((double)k + 1.0) - lf((double)(n - k) + 1.0);

@@ -165,9 +165,8 @@ struct PropArgs {
   Ctrl* ctrl;
 };
 
-// Register cap per model (M::kMinBlocks resident CTAs per SM): measured on
-// B200 — CRBD 4 (64 regs, no spills), SEIR 2 (its binomial code spills below
-// 128 registers).
+// Register cap per model (M::kMinBlocks resident CTAs per SM), measured on
+// B200: CRBD 4 (64 regs), SEIR 3 (80 regs; samplers out of line), ClaDS2 2.
 template <class M>
 __global__ void __launch_bounds__(kThreads, M::kMinBlocks) propagate_kernel(PropArgs a, ModelConst C) {
   __shared__ long long s_key[kThreads / 32];

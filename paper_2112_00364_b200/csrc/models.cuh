@@ -291,7 +291,7 @@ struct Clads2 {
 // ============================================================================
 struct Seir {
   static constexpr int kPlanes = 6;
-  static constexpr int kMinBlocks = 2;
+  static constexpr int kMinBlocks = 3;
   struct State { double lam_h, del_h, gam_h, lam_m, del_m, rho; int sh, eh, ih, rh, sm, em, im, t, pc; };
   __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
     uint4 v = ldp(P, st, 0, i); s.lam_h = lo_d(v); s.del_h = hi_d(v);
