@@ -91,6 +91,7 @@ struct smc_ctx {
   int world = 1, rank = 0;        // world = number of shards in the run
   int n_local_shards = 1;         // shards held by this handle
   int n_tiles = 0;
+  int items = kItems;             // particles per thread in a resampling tile
   unsigned long long seed = 0;
   ModelConst mc{};
   double* d_table = nullptr;
@@ -384,7 +385,8 @@ int common_init(smc_ctx* h, const smc_model* m, unsigned long long n_per, int wo
   h->rank = rank;
   h->n_local_shards = n_local_shards;
   h->seed = seed;
-  h->n_tiles = (int)((n_per + kTile - 1) / kTile);
+  h->items = n_per <= kSmallN ? kItemsSmall : kItems;
+  h->n_tiles = (int)((n_per + (unsigned long long)kThreads * h->items - 1) / ((unsigned long long)kThreads * h->items));
   CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   h->own_stream = true;
   if (!h->h_table.empty()) {
@@ -542,16 +544,26 @@ ResArgs res_args(smc_ctx* h, Shard& s, const double* lw, const uint4* src, int d
   a.ctrl = s.ctrl;
   return a;
 }
-void launch_anc_gather(smc_ctx* h, const ResArgs& a) {
+template <int IT>
+void launch_anc_gather_it(smc_ctx* h, const ResArgs& a) {
   const unsigned grid = (unsigned)h->n_tiles;
   switch (h->planes) {
-    case 1: anc_gather_kernel<1><<<grid, kThreads, 0, h->stream>>>(a); break;
-    case 2: anc_gather_kernel<2><<<grid, kThreads, 0, h->stream>>>(a); break;
-    case 4: anc_gather_kernel<4><<<grid, kThreads, 0, h->stream>>>(a); break;
-    case 6: anc_gather_kernel<6><<<grid, kThreads, 0, h->stream>>>(a); break;
-    case 8: anc_gather_kernel<8><<<grid, kThreads, 0, h->stream>>>(a); break;
-    default: anc_gather_kernel<0><<<grid, kThreads, 0, h->stream>>>(a); break;
+    case 1: anc_gather_kernel<1, IT><<<grid, kThreads, 0, h->stream>>>(a); break;
+    case 2: anc_gather_kernel<2, IT><<<grid, kThreads, 0, h->stream>>>(a); break;
+    case 4: anc_gather_kernel<4, IT><<<grid, kThreads, 0, h->stream>>>(a); break;
+    case 6: anc_gather_kernel<6, IT><<<grid, kThreads, 0, h->stream>>>(a); break;
+    case 8: anc_gather_kernel<8, IT><<<grid, kThreads, 0, h->stream>>>(a); break;
+    default: anc_gather_kernel<0, IT><<<grid, kThreads, 0, h->stream>>>(a); break;
   }
+}
+void launch_anc_gather(smc_ctx* h, const ResArgs& a) {
+  if (h->items == kItemsSmall) launch_anc_gather_it<kItemsSmall>(h, a);
+  else launch_anc_gather_it<kItems>(h, a);
+}
+void launch_reduce(smc_ctx* h, const ResArgs& a) {
+  const unsigned grid = (unsigned)((h->n_tiles + 1) / 2);     // two tiles per CTA
+  if (h->items == kItemsSmall) reduce_kernel<kItemsSmall><<<grid, kThreads, 0, h->stream>>>(a);
+  else reduce_kernel<kItems><<<grid, kThreads, 0, h->stream>>>(a);
 }
 void launch_finalize(smc_ctx* h, Shard& s) {
   FinArgs f;
@@ -578,8 +590,7 @@ int enqueue_epoch(smc_ctx* h) {
   int rc = allgather_rec(h, h->d_recA + cur * h->world, rec);
   if (rc) return rc;
   for (auto& s : h->shards) {
-    ResArgs a = res_args(h, s, s.lw, s.planes[cur], cur ^ 1);
-    reduce_kernel<<<h->n_tiles, kThreads, 0, h->stream>>>(a);
+    launch_reduce(h, res_args(h, s, s.lw, s.planes[cur], cur ^ 1));
   }
   CU(cudaGetLastError());
   rc = allgather_rec(h, h->d_recB + cur * h->world, rec);
@@ -1024,7 +1035,7 @@ int smc_resample_device(smc_handle h, const double* d_lw, const void* d_state_in
   const unsigned mgrid = (unsigned)std::min<unsigned long long>((h->n_per + kThreads - 1) / kThreads, 148ull * 8);
   max_kernel<<<mgrid, kThreads, 0, h->stream>>>(d_lw, h->n_per, h->d_recA, 1, 0, s.ctrl);
   ResArgs a = res_args(h, s, d_lw, (const uint4*)d_state_in, 1);
-  reduce_kernel<<<h->n_tiles, kThreads, 0, h->stream>>>(a);
+  launch_reduce(h, a);
   launch_anc_gather(h, a);
   launch_finalize(h, s);
   CU(cudaGetLastError());

@@ -24,8 +24,10 @@ namespace smc {
 typedef unsigned __int128 u128;
 
 constexpr int kThreads = 256;
-constexpr int kItems = 8;
-constexpr int kTile = kThreads * kItems;   // particles per resampling tile
+constexpr int kItems = 8;                  // particles per thread in a resampling tile (large N)
+constexpr int kItemsSmall = 2;             // ... below kSmallN particles per shard (more CTAs)
+constexpr unsigned long long kSmallN = 0;   // small tiles measured slower at 10^6 (per-CTA fixed costs dominate)
+constexpr int kTile = kThreads * kItems;
 
 // Record all-gathered after propagation (16 B per shard).
 struct RecA {
@@ -146,10 +148,35 @@ struct Grid {
   }
 };
 
+// q = rint(2^62 exp(x)), x = lw - m <= 0 (reading R9).  exp specialised to
+// this domain: q = 0 below x = -44 (2^62 e^-44 = 0.36 < 1/2); otherwise
+// x = k ln2 + r (Cody-Waite, |r| <= ln2/2), e^r by a degree-13 Horner
+// polynomial (truncation 6e-18), scaled by 2^(k+62) in [2^-2, 2^62] — no
+// over/underflow paths.  Within ~2 ulp of exp(); both resampling passes use
+// this one function, so W and the prefixes are consistent.
 __device__ __forceinline__ unsigned long long quantize(double lw, double m) {
-  if (lw == -INFINITY) return 0ull;
-  const double e = exp(lw - m);
-  return __double2ull_rn(e * 0x1p62);
+  const double x = lw - m;
+  if (!(x >= -44.0)) return 0ull;                   // also lw = -inf
+  const double k = rint(x * 1.4426950408889634074);
+  double r = fma(k, -6.93147180369123816490e-01, x);
+  r = fma(k, -1.90821492927058770002e-10, r);
+  double p = 1.6059043836821614599e-10;             // 1/13!
+  p = fma(p, r, 2.0876756987868098979e-09);         // 1/12!
+  p = fma(p, r, 2.5052108385441718775e-08);
+  p = fma(p, r, 2.7557319223985890653e-07);
+  p = fma(p, r, 2.7557319223985890653e-06);
+  p = fma(p, r, 2.4801587301587301587e-05);
+  p = fma(p, r, 1.9841269841269841270e-04);
+  p = fma(p, r, 1.3888888888888888889e-03);
+  p = fma(p, r, 8.3333333333333333333e-03);
+  p = fma(p, r, 4.1666666666666666667e-02);
+  p = fma(p, r, 1.6666666666666666667e-01);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int e2 = (int)k + 62 + 1023;                // 2^(k+62), k in [-64, 0]
+  const double scale = __hiloint2double(e2 << 20, 0);
+  return __double2ull_rn(p * scale);
 }
 
 // ============================================================================
@@ -285,43 +312,57 @@ __device__ __forceinline__ Global read_global(const RecA* A, int world) {
 // ============================================================================
 // reduce: per-tile u128 sums of q; the last CTA scans them
 // ============================================================================
+template <int ITEMS>
 __global__ void __launch_bounds__(kThreads) reduce_kernel(ResArgs a) {
-  __shared__ u128 s_w[kThreads / 32];
+  constexpr int kTile = kThreads * ITEMS;
+  constexpr int kItems = ITEMS;
+  constexpr int kTPB = 2;                               // tiles per CTA
+  __shared__ u128 s_w[kTPB][kThreads / 32];
   __shared__ unsigned s_ticket;
   if (*(volatile unsigned*)&a.ctrl->done) return;
   const unsigned par = a.ctrl->epoch & 1;
   const Global G = read_global(a.recA + par * a.world, a.world);
   if (!G.ok) return;
-  const unsigned long long base = (unsigned long long)blockIdx.x * kTile;
-  double v[kItems];
-  if (base + kTile <= a.n_local) {
-    // full tile: 16-byte loads, all issued before any math (MLP = kItems/2 per thread)
-    const double2* p = reinterpret_cast<const double2*>(a.lw + base);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double v[kTPB][kItems];
 #pragma unroll
-    for (int r = 0; r < kItems / 2; ++r) {
-      const double2 t = __ldg(p + r * kThreads + threadIdx.x);
-      v[2 * r] = t.x;
-      v[2 * r + 1] = t.y;
-    }
-  } else {
+  for (int tt = 0; tt < kTPB; ++tt) {                   // all loads first
+    const unsigned long long base = ((unsigned long long)blockIdx.x * kTPB + tt) * kTile;
+    if (base + kTile <= a.n_local) {
+      const double2* p = reinterpret_cast<const double2*>(a.lw + base);
 #pragma unroll
-    for (int r = 0; r < kItems; ++r) {
-      const unsigned long long i = base + (unsigned long long)r * kThreads + threadIdx.x;
-      v[r] = i < a.n_local ? __ldg(a.lw + i) : -INFINITY;
+      for (int r = 0; r < kItems / 2; ++r) {
+        const double2 t = __ldg(p + r * kThreads + threadIdx.x);
+        v[tt][2 * r] = t.x;
+        v[tt][2 * r + 1] = t.y;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < kItems; ++r) {
+        const unsigned long long i = base + (unsigned long long)r * kThreads + threadIdx.x;
+        v[tt][r] = i < a.n_local ? __ldg(a.lw + i) : -INFINITY;
+      }
     }
   }
-  u128 acc = 0;
 #pragma unroll
-  for (int r = 0; r < kItems; ++r) acc += quantize(v[r], G.m);
+  for (int tt = 0; tt < kTPB; ++tt) {
+    u128 acc = 0;
 #pragma unroll
-  for (int d = 16; d > 0; d >>= 1) acc += shfl_xor_u128(acc, d);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) s_w[warp] = acc;
+    for (int r = 0; r < kItems; ++r) acc += quantize(v[tt][r], G.m);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) acc += shfl_xor_u128(acc, d);
+    if (lane == 0) s_w[tt][warp] = acc;
+  }
   __syncthreads();
+  if (threadIdx.x < kTPB) {
+    const int tile = blockIdx.x * kTPB + threadIdx.x;
+    if (tile < a.n_tiles) {
+      u128 t = 0;
+      for (int w = 0; w < kThreads / 32; ++w) t += s_w[threadIdx.x][w];
+      a.tile_sum[tile] = t;
+    }
+  }
   if (threadIdx.x == 0) {
-    u128 t = 0;
-    for (int w = 0; w < kThreads / 32; ++w) t += s_w[w];
-    a.tile_sum[blockIdx.x] = t;
     __threadfence();
     s_ticket = atomicAdd(&a.ctrl->counter, 1u);
   }
@@ -342,10 +383,10 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(ResArgs a) {
     const u128 o = shfl_up_u128(incl, d);
     if (lane >= d) incl += o;
   }
-  if (lane == 31) s_w[warp] = incl;
+  if (lane == 31) s_w[0][warp] = incl;
   __syncthreads();
   u128 woff = 0;
-  for (int w = 0; w < warp; ++w) woff += s_w[w];
+  for (int w = 0; w < warp; ++w) woff += s_w[0][w];
   u128 run = woff + incl - local;
   for (int t = lo; t < hi; ++t) {
     a.tile_excl[t] = run;
@@ -382,8 +423,10 @@ __device__ __forceinline__ Grid make_grid(const ResArgs& a, const u128* B, unsig
   return gr;
 }
 
-template <int P>   // P = planes per particle; P <= 0: runtime a.planes
+template <int P, int ITEMS>   // P = planes per particle (<= 0: runtime a.planes)
 __global__ void __launch_bounds__(kThreads) anc_gather_kernel(ResArgs a) {
+  constexpr int kTile = kThreads * ITEMS;
+  constexpr int kItems = ITEMS;
   __shared__ double s_lw[kTile];
   __shared__ unsigned s_O[kTile];
   __shared__ u128 s_w[kThreads / 32];

@@ -285,3 +285,16 @@ def test_graph_and_step_modes_identical(smc):
     assert a.log_z == b.log_z
     np.testing.assert_array_equal(a.log_weights(), b.log_weights())
     np.testing.assert_array_equal(a.ancestors(), b.ancestors())
+
+
+@pytest.mark.parametrize("N", [(1 << 22) + 12345])
+def test_resampler_parity_large_tiles(smc, N):
+    """Above 2^22 particles the resampler uses 2048-particle tiles (8 per thread)."""
+    lw = inputs.resample_lw(N, 2.0, 0.1, seed=11)
+    st = inputs.state_bytes(N, 32, seed=12)
+    r = smc.Resampler(N, 32, seed=13)
+    anc, out, inc = r.host(lw, smc.aos_to_soa(st), epoch=3)
+    ref = oracle.resample(lw, seed=13, epoch=3)
+    np.testing.assert_array_equal(anc, ref["anc"])
+    assert inc == pytest.approx(ref["logz_inc"], rel=1e-13, abs=1e-13)
+    np.testing.assert_array_equal(smc.soa_to_aos(out), oracle.gather(st, ref["anc"]))
