@@ -44,6 +44,14 @@ WORKLOADS = {
 L2_BYTES = 126 * 2 ** 20
 
 
+def traffic(key):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(p)).get(key)
+    except Exception:
+        return None
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -78,7 +86,16 @@ class Clocks:
     def summary(self, dev=0):
         out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
         try:
-            rows = [r.split(", ") for r in open(self.path).read().strip().splitlines()]
+            text = open(self.path).read().strip()
+            if not text:
+                # timed region shorter than the sampling interval: one query right after it
+                q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                     "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                     "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+                text = subprocess.run(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader"],
+                                      capture_output=True, text=True).stdout.strip()
+                out["note"] = "sampled once right after the timed region (region < 100 ms)"
+            rows = [r.split(", ") for r in text.splitlines()]
             rows = [r for r in rows if r and r[0].strip() == str(dev)]
             sm = [float(r[1].split()[0]) for r in rows]
             mx = [float(r[2].split()[0]) for r in rows]
@@ -244,17 +261,23 @@ def bench_sweeps(args, wl, smc, torch, world, rank):
     # (host-stepped sweeps with the same seeds; not part of the headline time)
     h.set_timing(True)
     prop_ms = res_ms = 0.0
+    res_bytes = 0
     for k in range(args.steps):
         h.reset(1 + k)
         h.run()
         st = h.stats()
         prop_ms += st["ms_propagate"]
         res_ms += st["ms_resample"]
+        sb = st["state_bytes"]
+        n_loc = st["n_local"]
+        # algorithmic resample bytes of the sweep: per resample N*20 + S*(D + N),
+        # plus the final epoch's reduce (8 B/particle)
+        res_bytes += st["resamples"] * n_loc * (20 + sb) + sb * st["distinct"] + 8 * n_loc
     h.set_timing(False)
     # graph body = 2 epochs x (propagate, reduce, anc_gather, finalize) + set_condition
     E = steps_done // args.steps
     launches = args.steps * 9 * ((E + 1) // 2)
-    return dict(h=h, N=N, t_ms=t_ms, value=value, sweeps=sweeps_per_s, prop_ms=prop_ms,
+    return dict(h=h, N=N, t_ms=t_ms, value=value, sweeps=sweeps_per_s, prop_ms=prop_ms, res_bytes=res_bytes,
                 res_ms=res_ms, draws=draws, alive_steps=alive_steps, epochs=steps_done,
                 launches=launches, clocks=clk.summary(torch.cuda.current_device()),
                 logz=float(np.mean(logzs)))
@@ -310,7 +333,15 @@ def bench_resample(args, wl, smc, torch):
     times = [a.elapsed_time(b) for a, b in ev]
     D = r.distinct()
     alg = n * 20 + S * (D + n)
-    return dict(r=r, n=n, t_ms=float(np.mean(times)), alg_bytes=alg, D=D,
+    # per-kernel split (CUDA events around each kernel; separate, untimed passes)
+    r.set_timing(True)
+    for k in range(args.steps):
+        flush.zero_()
+        r.device(lw, st_in, st_out, anc, epoch=k)
+    torch.cuda.synchronize()
+    ms_k = [v / args.steps for v in r.stats()["ms_kernel"]]
+    r.set_timing(False)
+    return dict(r=r, n=n, t_ms=float(np.mean(times)), alg_bytes=alg, D=D, ms_kernel=ms_k,
                 clocks=clk.summary(torch.cuda.current_device()))
 
 
@@ -352,16 +383,28 @@ def run_ours(args, wl):
     hbm_peak = pk["hbm_gbs"]
     if wl["model"] == "resample":
         r = bench_resample(args, wl, smc, torch)
-        achieved = r["alg_bytes"] / (r["t_ms"] / 1e-3) / 1e9 * 1e-6 * 1e6
         achieved = r["alg_bytes"] / (r["t_ms"] * 1e-3) / 1e9
+        n, D = r["n"], r["D"]
+        g_bytes = n * 12 + 64 * (D + n)          # anc_gather: lw read, anc write, states
+        g_ms = r["ms_kernel"][2]
+        g_ach = g_bytes / (g_ms * 1e-3) / 1e9
+        tr = traffic(f"resample:{n}:anc_gather")
         line = dict(metric="resample effective HBM GB/s (B_alg = N*20 + 64*(D+N))", value=achieved,
                     unit="GB/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
                     ms_per_step=r["t_ms"], higher_is_better=True, scaling="weak", vs_baseline=None,
                     dtype="f64/u128", data="synthetic",
                     config=dict(workload="resample", desc=wl["desc"], n_per_gpu=r["n"],
                                 state_bytes=64, sigma=args.sigma, l2="flushed between steps"),
-                    roofline=dict(bound="hbm", achieved=achieved, peak=hbm_peak, unit="GB/s",
-                                  frac=achieved / hbm_peak, traffic=None, peak_source=pk_kind),
+                    roofline=dict(bound="hbm", kernel="anc_gather_kernel (ancestors + fused gather)",
+                                  achieved=g_ach, peak=hbm_peak, unit="GB/s", frac=g_ach / hbm_peak,
+                                  traffic=(tr["bytes"] if tr else None),
+                                  algorithmic_bytes=g_bytes, ms=g_ms, peak_source=pk_kind),
+                    chain_roofline=dict(bound="hbm", achieved=achieved, peak=hbm_peak, unit="GB/s",
+                                        frac=achieved / hbm_peak, algorithmic_bytes=r["alg_bytes"],
+                                        note="max + reduce + anc_gather + finalize; B_alg excludes "
+                                             "the standalone max pass (8 B/particle)"),
+                    kernel_ms=dict(zip(["max", "reduce", "anc_gather", "finalize"], r["ms_kernel"])),
+                    distinct_ancestors=D,
                     gpu_launches=5 * args.steps, clocks=r["clocks"])
         if rank == 0:
             print(json.dumps(line), flush=True)
@@ -387,11 +430,18 @@ def run_ours(args, wl):
                 phase_ms=dict(propagate=r["prop_ms"] / args.steps, resample=r["res_ms"] / args.steps,
                               propagate_share=prop_frac),
                 draws_per_particle_step=r["draws"] / max(r["alive_steps"], 1),
+                resample_roofline=dict(bound="hbm", achieved=r["res_bytes"] / (r["res_ms"] * 1e-3) / 1e9,
+                                       peak=hbm_peak, unit="GB/s",
+                                       frac=r["res_bytes"] / (r["res_ms"] * 1e-3) / 1e9 / hbm_peak,
+                                       note="reduce + anc_gather + finalize per epoch at this N "
+                                            "(latency-bound at 10^6; see workload 'resample')"),
                 roofline=dict(bound="alu",
                               kernel=("propagate_lr_kernel" if args.rng == "lineage" and wl["model"] != "seir"
                                       else "propagate_kernel") + f"<{wl['model']}>",
                               achieved=draw_rate, peak=draw_peak, unit="Gdraws/s",
-                              frac=draw_rate / draw_peak, traffic=None,
+                              frac=draw_rate / draw_peak,
+                              traffic=((traffic(f"{wl['model']}:{N}:propagate_lr_kernel") or {}).get("bytes")
+                                       if args.rng == "lineage" else None),
                               peak_source=f"derived: 148 SM x 128 lanes x {f_max/1e6:.0f} MHz / 34 instr per uniform (DESIGN.md s7)"),
                 gpu_launches=r["launches"], clocks=r["clocks"])
     if rank == 0 and not args.no_e2e and world == 1:

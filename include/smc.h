@@ -121,6 +121,10 @@ typedef struct {
   uint64_t side_roots;              /* lineage-keyed kernels: hidden events (side-tree roots) */
   uint32_t max_rounds;              /* ... longest cooperative phase of a batch (rounds)      */
   uint32_t max_side_nodes;          /* ... largest side-tree node count of one particle-step  */
+  uint64_t distinct;                /* distinct ancestors, summed over the resamples since
+                                       reset (per call for smc_resample_*)                   */
+  double ms_kernel[4];              /* resample-only path with timing on: CUDA-event ms of
+                                       max, reduce, anc_gather, finalize (accumulated)       */
 } smc_stats_t;
 
 /* --- lifetime --------------------------------------------------------------- */

@@ -55,7 +55,8 @@ class smc_stats_t(C.Structure):
                 ("shards", C.c_int32), ("state_bytes", C.c_uint32), ("done", C.c_uint32),
                 ("draws", C.c_uint64), ("ms_propagate", C.c_double), ("ms_resample", C.c_double),
                 ("timed_epochs", C.c_uint64), ("side_roots", C.c_uint64),
-                ("max_rounds", C.c_uint32), ("max_side_nodes", C.c_uint32)]
+                ("max_rounds", C.c_uint32), ("max_side_nodes", C.c_uint32),
+                ("distinct", C.c_uint64), ("ms_kernel", C.c_double * 4)]
 
 
 ALLGATHER_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)
@@ -272,7 +273,9 @@ class Smc:
     def stats(self):
         s = smc_stats_t()
         _check(self.h, _lib.smc_stats(self.h, C.byref(s)))
-        return {k: getattr(s, k) for k, _ in smc_stats_t._fields_}
+        d = {k: getattr(s, k) for k, _ in smc_stats_t._fields_}
+        d["ms_kernel"] = list(d["ms_kernel"])
+        return d
 
 
 class Resampler:
@@ -315,6 +318,16 @@ class Resampler:
                                               anc.ctypes.data_as(C.POINTER(C.c_uint32)), int(epoch),
                                               C.byref(inc)))
         return anc, out, inc.value
+
+    def set_timing(self, on=True):
+        _check(self.h, _lib.smc_set_timing(self.h, 1 if on else 0))
+
+    def stats(self):
+        s = smc_stats_t()
+        _check(self.h, _lib.smc_stats(self.h, C.byref(s)))
+        d = {k: getattr(s, k) for k, _ in smc_stats_t._fields_}
+        d["ms_kernel"] = list(d["ms_kernel"])
+        return d
 
     def distinct(self):
         v = C.c_uint64(0)

@@ -114,6 +114,8 @@ struct smc_ctx {
   bool started = false;
   bool timing = false;            // per-phase CUDA-event timing
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t rev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};   // resample-only path
+  double ms_kernel[4] = {0, 0, 0, 0};   // max, reduce, anc_gather, finalize (resample-only path)
   double ms_propagate = 0.0, ms_resample = 0.0;
   unsigned long long timed_epochs = 0;
   bool use_graph = true;          // whole run as one graph launch (WHILE conditional node)
@@ -359,6 +361,7 @@ int reset_device(smc_ctx* h) {
   CU(cudaStreamSynchronize(h->stream));
   std::memset(h->h_ctrl, 0, sizeof(Ctrl));
   h->ms_propagate = h->ms_resample = 0.0;
+  for (double& v : h->ms_kernel) v = 0.0;
   h->timed_epochs = 0;
   h->enq = 0;
   h->started = false;
@@ -842,6 +845,7 @@ void smc_destroy(smc_handle h) {
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   if (h->h_ctrl) cudaFreeHost(h->h_ctrl);
   for (auto& e : h->ev) if (e) cudaEventDestroy(e);
+  for (auto& e : h->rev) if (e) cudaEventDestroy(e);
   if (h->nccl && g_nccl.CommDestroy) g_nccl.CommDestroy(h->nccl);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
@@ -869,8 +873,10 @@ int smc_set_graph(smc_handle h, int32_t on) {
 
 int smc_set_timing(smc_handle h, int32_t on) {
   if (!h) return fail(h, SMC_EINVAL, "NULL handle");
-  if (on && !h->ev[0])
+  if (on && !h->ev[0]) {
     for (auto& e : h->ev) CU(cudaEventCreate(&e));
+    for (auto& e : h->rev) CU(cudaEventCreate(&e));
+  }
   h->timing = on != 0;
   return SMC_OK;
 }
@@ -993,14 +999,16 @@ int smc_stats(smc_handle h, smc_stats_t* out) {
   out->ms_propagate = h->ms_propagate;
   out->ms_resample = h->ms_resample;
   out->timed_epochs = h->timed_epochs;
+  for (int k = 0; k < 4; ++k) out->ms_kernel[k] = h->ms_kernel[k];
   if (h->stream && cudaStreamSynchronize(h->stream) == cudaSuccess) {
-    unsigned long long alive = 0, ovf = 0, fe = ~0ull, drw = 0, roots = 0;
+    unsigned long long alive = 0, ovf = 0, fe = ~0ull, drw = 0, roots = 0, dist = 0;
     unsigned mr = 0, mn = 0;
     for (auto& s : h->shards) {
       Ctrl c;
       if (cudaMemcpy(&c, s.ctrl, sizeof(c), cudaMemcpyDeviceToHost) != cudaSuccess) break;
       alive += c.alive_steps; ovf += c.overflow; fe = std::min(fe, c.first_err); drw += c.draws;
       roots += c.side_roots; mr = std::max(mr, c.max_rounds); mn = std::max(mn, c.max_side_nodes);
+      dist += c.distinct;
       out->epochs = c.epochs; out->resamples = c.resamples; out->done = c.done;
       if (c.status && !out->status) out->status = status_of(c);
     }
@@ -1008,6 +1016,7 @@ int smc_stats(smc_handle h, smc_stats_t* out) {
     out->overflow = ovf;
     out->draws = drw;
     out->side_roots = roots;
+    out->distinct = dist;
     out->max_rounds = mr;
     out->max_side_nodes = mn;
     out->first_error_particle = fe == ~0ull ? -1 : (int64_t)fe;
@@ -1033,13 +1042,26 @@ int smc_resample_device(smc_handle h, const double* d_lw, const void* d_state_in
   CU(cudaMemcpyAsync(s.d_dst_anc, &d_anc, sizeof(d_anc), cudaMemcpyHostToDevice, h->stream));
   prep_resample_kernel<<<1, 32, 0, h->stream>>>(s.ctrl, h->d_recA, h->d_recB, 1, 0, epoch);
   const unsigned mgrid = (unsigned)std::min<unsigned long long>((h->n_per + kThreads - 1) / kThreads, 148ull * 8);
+  if (h->timing) CU(cudaEventRecord(h->rev[0], h->stream));
   max_kernel<<<mgrid, kThreads, 0, h->stream>>>(d_lw, h->n_per, h->d_recA, 1, 0, s.ctrl);
+  if (h->timing) CU(cudaEventRecord(h->rev[1], h->stream));
   ResArgs a = res_args(h, s, d_lw, (const uint4*)d_state_in, 1);
   launch_reduce(h, a);
+  if (h->timing) CU(cudaEventRecord(h->rev[2], h->stream));
   launch_anc_gather(h, a);
+  if (h->timing) CU(cudaEventRecord(h->rev[3], h->stream));
   launch_finalize(h, s);
+  if (h->timing) CU(cudaEventRecord(h->rev[4], h->stream));
   CU(cudaGetLastError());
   h->started = true;
+  if (h->timing) {
+    CU(cudaEventSynchronize(h->rev[4]));
+    for (int k = 0; k < 4; ++k) {
+      float ms = 0.f;
+      CU(cudaEventElapsedTime(&ms, h->rev[k], h->rev[k + 1]));
+      h->ms_kernel[k] += ms;
+    }
+  }
   if (logz_inc) {
     CU(cudaMemcpyAsync(h->h_ctrl, s.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));
