@@ -305,6 +305,45 @@ def e2e_sweeps(args, wl, smc, torch, N, k_steps):
     return dict(t=float(np.mean(ts)), h2d=h2d, d2h=d2h, logz=lz)
 
 
+def bench_resample_sharded(args, wl, smc, torch, world, rank):
+    """configs[4] at N GPUs: each rank holds n particles; one global resampling
+    step of the handles' own buffers per timed step (all-gathers over NCCL,
+    migration by peer stores)."""
+    from paper_2112_00364_b200 import dist as sdist
+    n = args.n or wl["n"]
+    S = 64
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev)
+    g.manual_seed(4 + 1000 * rank)
+    lw = torch.randn(n, generator=g, device=dev, dtype=torch.float64) * args.sigma
+    st = torch.randint(0, 2 ** 31 - 1, (S // 4 * n,), generator=g, device=dev, dtype=torch.int32)
+    stream = torch.cuda.current_stream()
+    h = sdist.sharded(smc.Model.resample_bench(S), n, seed=4, stream=stream)
+    h.load(lw, st)
+    del st
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+    for w in range(args.warmup):
+        h.resample_step(w)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    barrier(torch, world)
+    dist_d = 0
+    with Clocks(os.path.join(args.out, f"clocks_rank{rank}.csv")) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            h.resample_step(args.warmup + k)
+            ev[k][1].record(stream)
+            dist_d += h.distinct()
+        torch.cuda.synchronize()
+    barrier(torch, world)
+    t_ms = max_over_ranks(torch, world, sum(a.elapsed_time(b) for a, b in ev))
+    D = sum_over_ranks(torch, world, dist_d) / args.steps
+    alg = world * n * 20 + S * (D + world * n)
+    return dict(n=n, t_ms=t_ms / args.steps, alg_bytes=alg, D=D, clocks=clk.summary(torch.cuda.current_device()))
+
+
 def bench_resample(args, wl, smc, torch):
     n = args.n or wl["n"]
     S = 64
@@ -381,6 +420,23 @@ def run_ours(args, wl):
     import paper_2112_00364_b200 as smc
     pk, pk_kind = peaks()
     hbm_peak = pk["hbm_gbs"]
+    if wl["model"] == "resample" and world > 1:
+        r = bench_resample_sharded(args, wl, smc, torch, world, rank)
+        achieved = r["alg_bytes"] / (r["t_ms"] * 1e-3) / 1e9
+        line = dict(metric="resample effective HBM GB/s (B_alg = N*20 + 64*(D+N), all GPUs)",
+                    value=achieved, unit="GB/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
+                    ms_per_step=r["t_ms"], higher_is_better=True, scaling="weak", vs_baseline=None,
+                    dtype="f64/u128", data="synthetic",
+                    config=dict(workload="resample", desc=wl["desc"], n_per_gpu=r["n"], state_bytes=64,
+                                sigma=args.sigma, parallelism=f"global resampling over {world} GPUs",
+                                l2="flushed between steps"),
+                    roofline=dict(bound="hbm", achieved=achieved / world, peak=hbm_peak, unit="GB/s",
+                                  frac=achieved / world / hbm_peak, traffic=None,
+                                  note="per GPU; chain incl. NCCL all-gathers and NVLink migration"),
+                    gpu_launches=(5 * world + 0) * args.steps, clocks=r["clocks"])
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        return
     if wl["model"] == "resample":
         r = bench_resample(args, wl, smc, torch)
         achieved = r["alg_bytes"] / (r["t_ms"] * 1e-3) / 1e9

@@ -234,6 +234,16 @@ int smc_resample_device(smc_handle h, const double* d_lw, const void* d_state_in
 int smc_resample_host(smc_handle h, const double* lw, const void* state_in, void* state_out,
                       uint32_t* anc, uint32_t epoch, double* logz_inc);
 
+/* Resampling of the handle's OWN buffers, global across shards/ranks (the
+ * multi-GPU form of configs[4]).  smc_load copies n_local log-weights and the
+ * SoA state (plane-major per shard) into the handle (device_ptrs != 0: device
+ * pointers, else host); smc_resample_step then runs max, reduce, the two
+ * all-gathers, anc_gather with peer-store migration, the barrier and
+ * finalize, and swaps buffers; smc_state / smc_ancestors read the result.
+ * Enqueued on the handle's stream (host-staged comm synchronises). */
+int smc_load(smc_handle h, const double* lw, const void* state, int32_t device_ptrs);
+int smc_resample_step(smc_handle h, uint32_t epoch);
+
 /* Number of distinct ancestors in the last smc_resample_* call (for the
  * algorithmic-bytes count); synchronises. */
 int smc_last_distinct(smc_handle h, uint64_t* out);

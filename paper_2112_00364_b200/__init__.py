@@ -97,6 +97,8 @@ _sig = {
     "smc_resample_host": ([H, C.POINTER(C.c_double), C.c_void_p, C.c_void_p,
                            C.POINTER(C.c_uint32), C.c_uint32, C.POINTER(C.c_double)], C.c_int),
     "smc_last_distinct": ([H, C.POINTER(C.c_uint64)], C.c_int),
+    "smc_load": ([H, C.c_void_p, C.c_void_p, C.c_int32], C.c_int),
+    "smc_resample_step": ([H, C.c_uint32], C.c_int),
     "smc_plan_ranges": ([C.POINTER(C.c_uint64), C.c_int32, C.c_uint64, C.c_uint64,
                          C.POINTER(C.c_uint64)], C.c_int),
 }
@@ -263,6 +265,26 @@ class Smc:
         out = np.empty((self.n, F), dtype=np.float64)
         _check(self.h, _lib.smc_fields(self.h, _dptr(out), out.size))
         return out
+
+    def load(self, lw, state):
+        """RESAMPLE_BENCH handles: numpy arrays (host) or torch CUDA tensors."""
+        dev = hasattr(lw, "data_ptr")
+        lp = lw.data_ptr() if dev else np.ascontiguousarray(lw, dtype=np.float64).ctypes.data
+        if not dev:
+            self._load_keep = (np.ascontiguousarray(lw, dtype=np.float64),
+                               np.ascontiguousarray(state, dtype=np.uint8))
+            lp, sp = self._load_keep[0].ctypes.data, self._load_keep[1].ctypes.data
+        else:
+            sp = state.data_ptr()
+        _check(self.h, _lib.smc_load(self.h, C.c_void_p(lp), C.c_void_p(sp), 1 if dev else 0))
+
+    def resample_step(self, epoch):
+        _check(self.h, _lib.smc_resample_step(self.h, int(epoch)))
+
+    def distinct(self):
+        v = C.c_uint64(0)
+        _check(self.h, _lib.smc_last_distinct(self.h, C.byref(v)))
+        return v.value
 
     def state(self):
         st = self.stats()

@@ -949,6 +949,10 @@ int smc_log_weights(smc_handle h, double* out, uint64_t n) {
 }
 
 static int current_parity(smc_ctx* h) {
+  if (h->kind == SMC_RESAMPLE_BENCH) {
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    return (int)(h->enq & 1);
+  }
   if (read_ctrl(h)) return -1;
   return (int)(h->h_ctrl->resamples & 1);
 }
@@ -1140,12 +1144,56 @@ int smc_plan_ranges(const uint64_t* w_lohi, int32_t world, uint64_t n_per, uint6
   return SMC_OK;
 }
 
+int smc_load(smc_handle h, const double* lw, const void* state, int32_t device_ptrs) {
+  if (!h || !lw || !state) return fail(h, SMC_EINVAL, "NULL argument");
+  if (h->kind != SMC_RESAMPLE_BENCH) return fail(h, SMC_ESTATE, "smc_load needs a RESAMPLE_BENCH handle");
+  const size_t per = (size_t)h->planes * 16 * h->n_per;
+  const int cur = (int)(h->enq & 1);
+  const cudaMemcpyKind kind = device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  for (size_t i = 0; i < h->shards.size(); ++i) {
+    CU(cudaMemcpyAsync(h->shards[i].lw, lw + i * h->n_per, h->n_per * sizeof(double), kind, h->stream));
+    CU(cudaMemcpyAsync(h->shards[i].planes[cur], (const char*)state + i * per, per, kind, h->stream));
+  }
+  CU(cudaStreamSynchronize(h->stream));
+  return SMC_OK;
+}
+
+int smc_resample_step(smc_handle h, uint32_t epoch) {
+  if (!h || h->kind != SMC_RESAMPLE_BENCH) return fail(h, SMC_ESTATE, "needs a RESAMPLE_BENCH handle");
+  if (!h->ipc_ready) return fail(h, SMC_ESTATE, "smc_ipc_import has not been called");
+  const int cur = (int)(h->enq & 1);
+  const unsigned par = epoch & 1;
+  for (auto& s : h->shards) {
+    prep_resample_kernel<<<1, 32, 0, h->stream>>>(s.ctrl, h->d_recA, h->d_recB, h->world, s.id, epoch);
+    const unsigned mgrid = (unsigned)std::min<unsigned long long>((h->n_per + kThreads - 1) / kThreads, 148ull * 8);
+    max_kernel<<<mgrid, kThreads, 0, h->stream>>>(s.lw, h->n_per, h->d_recA, h->world, s.id, s.ctrl);
+  }
+  CU(cudaGetLastError());
+  int rc = allgather_rec(h, h->d_recA + par * h->world, 16);
+  if (rc) return rc;
+  for (auto& s : h->shards) launch_reduce(h, res_args(h, s, s.lw, s.planes[cur], cur ^ 1));
+  rc = allgather_rec(h, h->d_recB + par * h->world, 16);
+  if (rc) return rc;
+  for (auto& s : h->shards) launch_anc_gather(h, res_args(h, s, s.lw, s.planes[cur], cur ^ 1));
+  rc = barrier(h);
+  if (rc) return rc;
+  for (auto& s : h->shards) launch_finalize(h, s);
+  CU(cudaGetLastError());
+  h->enq++;
+  h->started = true;
+  return SMC_OK;
+}
+
 int smc_last_distinct(smc_handle h, uint64_t* out) {
   if (!h || !out) return fail(h, SMC_EINVAL, "NULL argument");
   CU(cudaStreamSynchronize(h->stream));
-  Ctrl c;
-  CU(cudaMemcpy(&c, h->shards[0].ctrl, sizeof(c), cudaMemcpyDeviceToHost));
-  *out = c.distinct;
+  unsigned long long d = 0;
+  for (auto& sh : h->shards) {
+    Ctrl c;
+    CU(cudaMemcpy(&c, sh.ctrl, sizeof(c), cudaMemcpyDeviceToHost));
+    d += c.distinct;
+  }
+  *out = d;
   return SMC_OK;
 }
 

@@ -61,9 +61,34 @@ def gpu_worker(rank, world, port, outdir, n_per, seed, lineage):
     m = smc.Model.crbd(inputs.tree("tree90"), lineage=lineage)
     h = sdist.ShardedSmc(m, n_per, seed, comm="host")
     rc = h.run_status()
-    np.save(os.path.join(outdir, f"g{rank}.npy"),
-            np.array([rc, h.log_z, h.ancestors(), h.log_weights(), h.fields(), h.stats()], dtype=object),
-            allow_pickle=True)
+    res = np.empty(6, dtype=object)
+    res[:] = [rc, h.log_z, h.ancestors(), h.log_weights(), h.fields(), h.stats()]
+    np.save(os.path.join(outdir, f"g{rank}.npy"), res, allow_pickle=True)
+    h.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def gpu_resample_worker(rank, world, port, outdir, n_per):
+    """configs[4] across processes on one GPU: host comm + CUDA IPC."""
+    dist = init(rank, world, port)
+    import torch
+    torch.cuda.set_device(0)
+    import inputs
+    import paper_2112_00364_b200 as smc
+    from paper_2112_00364_b200 import dist as sdist
+    S = 64
+    N = world * n_per
+    lw = inputs.resample_lw(N, 2.0, 0.2, seed=41)[rank * n_per:(rank + 1) * n_per]
+    st = inputs.state_bytes(N, S, seed=42)[rank * n_per:(rank + 1) * n_per]
+    h = sdist.ShardedSmc(smc.Model.resample_bench(S), n_per, 7, comm="host")
+    h.load(lw, smc.aos_to_soa(st).ravel())
+    h.resample_step(0)
+    h.resample_step(1)
+    out = smc.soa_to_aos(h.state().reshape(S // 16, n_per, 16))
+    res = np.empty(2, dtype=object)
+    res[0], res[1] = h.ancestors(), out
+    np.save(os.path.join(outdir, f"rs{rank}.npy"), res, allow_pickle=True)
     h.close()
     dist.barrier()
     dist.destroy_process_group()

@@ -298,3 +298,36 @@ def test_resampler_parity_large_tiles(smc, N):
     np.testing.assert_array_equal(anc, ref["anc"])
     assert inc == pytest.approx(ref["logz_inc"], rel=1e-13, abs=1e-13)
     np.testing.assert_array_equal(smc.soa_to_aos(out), oracle.gather(st, ref["anc"]))
+
+
+# ------------------------------------------------------------- resampling of own buffers, sharded
+def _soa_shards(smc, st, shards):
+    n = st.shape[0] // shards
+    return np.concatenate([smc.aos_to_soa(st[g * n:(g + 1) * n]).ravel() for g in range(shards)])
+
+
+def _aos_shards(smc, raw, shards, S):
+    per = raw.size // shards
+    n = per // S
+    return np.concatenate([smc.soa_to_aos(raw[g * per:(g + 1) * per].reshape(S // 16, n, 16))
+                           for g in range(shards)])
+
+
+@pytest.mark.parametrize("shards", [1, 2, 3])
+def test_resample_step_sharded(smc, shards):
+    """configs[4] across shards: two consecutive global resampling steps of the
+    handle's own buffers equal the oracle's, whatever the shard count."""
+    S, n = 64, 5003
+    N = shards * n
+    lw = inputs.resample_lw(N, 2.0, 0.2, seed=21)
+    st = inputs.state_bytes(N, S, seed=22)
+    h = smc.Smc(smc.Model.resample_bench(S), N, 31, shards=shards)
+    h.load(lw, _soa_shards(smc, st, shards))
+    ref_st = st
+    for epoch in (0, 1):
+        h.resample_step(epoch)
+        ref = oracle.resample(lw, seed=31, epoch=epoch)
+        ref_st = oracle.gather(ref_st, ref["anc"])
+        np.testing.assert_array_equal(h.ancestors(), ref["anc"])
+        assert h.distinct() == len(np.unique(ref["anc"]))
+    np.testing.assert_array_equal(_aos_shards(smc, h.state(), shards, S), ref_st)
