@@ -79,6 +79,7 @@ struct OwnerClads2 { double eps, alpha, sigma, pb; };
 // CRBD under §R-18
 // ---------------------------------------------------------------------------
 struct CrbdLR {
+  static constexpr int kLRMinBlocks = SMC_LR_MINB;   // 64 registers at 128 threads
   typedef Crbd::State State;
   typedef OwnerCrbd Owner;
   static constexpr int kPlanes = Crbd::kPlanes;
@@ -145,6 +146,10 @@ struct CrbdLR {
 // ClaDS2 under §R-18 (with the §R-14b rate guard)
 // ---------------------------------------------------------------------------
 struct Clads2LR {
+#ifndef SMC_LR_MINB_CLADS2
+#define SMC_LR_MINB_CLADS2 4
+#endif
+  static constexpr int kLRMinBlocks = SMC_LR_MINB_CLADS2;   // larger state: avoid spills
   typedef Clads2::State State;
   typedef OwnerClads2 Owner;
   static constexpr int kPlanes = Clads2::kPlanes;
@@ -236,7 +241,7 @@ struct Clads2LR {
 
 // ---------------------------------------------------------------------------
 template <class M>
-__global__ void __launch_bounds__(kLRThreads, SMC_LR_MINB) propagate_lr_kernel(LRArgs a, ModelConst C) {
+__global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kernel(LRArgs a, ModelConst C) {
   __shared__ int s_cnt[kLRThreads];          // tasks in owner o's segment
   __shared__ int s_sel[kLRThreads];          // this round: lane -> task slot (owner-written)
   __shared__ int s_ovtop;                     // overflow stack top
