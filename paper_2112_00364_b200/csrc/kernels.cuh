@@ -238,8 +238,11 @@ __global__ void __launch_bounds__(kThreads, M::kMinBlocks) propagate_kernel(Prop
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) { s_key[warp] = key; s_ovf[warp] = ovf; s_drw[warp] = drw; }
   if (dg.overflow || bad) atomicMin(&a.ctrl->first_err, a.shard_base + i);
+  __syncwarp();   // bar.red needs a converged warp (synccheck)
   const int n_end = __syncthreads_count(end_alive);
+  __syncwarp();   // bar.red needs a converged warp (synccheck)
   const int n_start = __syncthreads_count(start_alive);
+  __syncwarp();   // bar.red needs a converged warp (synccheck)
   const int any_bad = __syncthreads_or(bad);
   if (threadIdx.x == 0) {
     long long k = s_key[0];

@@ -326,6 +326,7 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
     const int warp_id = tid >> 5, lane_id = tid & 31;
     for (;;) {
       const int c = s_cnt[tid];
+      __syncwarp();   // bar.red needs a converged warp (synccheck)
       const int active = __syncthreads_count(c > 0);
       const int ov = s_ovtop;
       if (active == 0 && ov == 0) break;
@@ -377,17 +378,19 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
       s_cnt[tid] = c - m;
       if (tid == 0) s_ovtop = ov - min(ov, kLRThreads - T);
       __syncthreads();
-      if (have && s_dead[o] == 0) {
+      // s_dead is a sticky flag (0 -> nonzero, never back): written and read
+      // with shared-memory atomics; a stale 0 only costs one pruned-late node
+      if (have && atomicAdd(&s_dead[o], 0) == 0) {
         const unsigned cnt = atomicAdd(&s_nodes[o], 1u) + 1u;
         if (cnt > kSideNodeCap) {
-          s_dead[o] = 2;
+          atomicCAS(&s_dead[o], 0, 2);
         } else {
           const uint32_t n_owner = (uint32_t)(p.shard_base + (unsigned long long)batch * kLRThreads + o);
           drw += 2;
           NodeOut out;
           const int res = M::node(ts, tl, tidv, s_own[o], n_owner, epoch, seed, rho, out);
           if (res == NODE_DETECTED) {
-            if (s_dead[o] == 0) s_dead[o] = 1;
+            atomicCAS(&s_dead[o], 0, 1);
           } else if (res == NODE_BIRTH) {
             push_task(o, out.s2, out.lb, out.idb);
             push_task(o, out.s2, out.la, out.ida);     // first daughter on top (DFS order)
@@ -440,7 +443,9 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
     s_acc[1][warp] = n_start;
     s_acc[2][warp] = drw;
   }
+  __syncwarp();   // bar.red needs a converged warp (synccheck)
   const int any_bad = __syncthreads_or(bad);
+  __syncwarp();   // bar.red needs a converged warp (synccheck)
   const int any_ovf = __syncthreads_or(ovf != 0);
   unsigned long long ovf_sum = ovf;
   (void)ovf_sum;
