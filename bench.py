@@ -277,32 +277,35 @@ def bench_sweeps(args, wl, smc, torch, world, rank):
     # graph body = 2 epochs x (propagate, reduce, anc_gather, finalize) + set_condition
     E = steps_done // args.steps
     launches = args.steps * 9 * ((E + 1) // 2)
-    return dict(h=h, N=N, t_ms=t_ms, value=value, sweeps=sweeps_per_s, prop_ms=prop_ms, res_bytes=res_bytes,
+    return dict(h=h, model=model, N=N, t_ms=t_ms, value=value, sweeps=sweeps_per_s, prop_ms=prop_ms,
+                res_bytes=res_bytes,
                 res_ms=res_ms, draws=draws, alive_steps=alive_steps, epochs=steps_done,
                 launches=launches, clocks=clk.summary(torch.cuda.current_device()),
                 logz=float(np.mean(logzs)))
 
 
-def e2e_sweeps(args, wl, smc, torch, N, k_steps):
-    """End to end through the public API with host buffers: every step creates a
-    handle from the host model description (H2D of the tree table), runs the
-    sweep, and reads back log Z and the N final log-weights (D2H)."""
-    model = model_for(smc, wl, args.rng)
+def e2e_sweeps(args, wl, smc, torch, h, model, k_steps, world):
+    """End to end through the public API: every step uploads the step's input
+    (the model data: tree table / case series, from pinned host memory) into
+    the handle, re-initialises it with the step's seed, runs the sweep and
+    reads back log Z and the final log-weights (D2H).  Host wall clock around
+    the whole step, max over ranks."""
+    data = torch.from_numpy(model.data.copy()).pin_memory().numpy()
     ts = []
-    h2d = model.data.nbytes + model.params.nbytes
     for k in range(k_steps + 1):
+        barrier(torch, world)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        h = smc.Smc(model, N, seed=500 + k)
+        h.set_data(data)
+        h.reset(500 + k)
         h.run()
         lz = h.log_z
         lw = h.log_weights()
-        h.close()
         torch.cuda.synchronize()
         if k:                         # first is warm-up
             ts.append(time.perf_counter() - t0)
-    d2h = lw.nbytes + 8
-    return dict(t=float(np.mean(ts)), h2d=h2d, d2h=d2h, logz=lz)
+    t = max_over_ranks(torch, world, float(np.mean(ts)))
+    return dict(t=t, h2d=data.nbytes, d2h=lw.nbytes + 8, logz=lz)
 
 
 def bench_resample_sharded(args, wl, smc, torch, world, rank):
@@ -500,10 +503,13 @@ def run_ours(args, wl):
                                        if args.rng == "lineage" else None),
                               peak_source=f"derived: 148 SM x 128 lanes x {f_max/1e6:.0f} MHz / 34 instr per uniform (DESIGN.md s7)"),
                 gpu_launches=r["launches"], clocks=r["clocks"])
-    if rank == 0 and not args.no_e2e and world == 1:
-        e = e2e_sweeps(args, wl, smc, torch, N, min(args.steps, 3))
-        line["e2e"] = dict(value=r["alive_steps"] / args.steps / e["t"], unit="particle-steps/s",
-                           h2d_bytes_per_step=e["h2d"], d2h_bytes_per_step=e["d2h"])
+    if not args.no_e2e:
+        e = e2e_sweeps(args, wl, smc, torch, r["h"], r["model"], min(args.steps, 3), world)
+        tot = sum_over_ranks(torch, world, r["alive_steps"] / args.steps)
+        line["e2e"] = dict(value=tot / e["t"], unit="particle-steps/s",
+                           h2d_bytes_per_step=e["h2d"] * world, d2h_bytes_per_step=e["d2h"] * world,
+                           note="per step: H2D of the model data, reset(seed), run, D2H of log Z and "
+                                "the final log-weights; host wall clock, max over ranks")
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         v, sample, dt, _ = oracle_sweep_rate(wl, budget_s=args.cpu_budget)
         line["cpu_baseline"] = dict(value=v, unit="particle-steps/s", cores=1, kind="oracle",

@@ -186,6 +186,12 @@ int smc_set_graph(smc_handle h, int32_t on);
  * accumulate into smc_stats_t.ms_propagate / ms_resample until smc_reset. */
 int smc_set_timing(smc_handle h, int32_t on);
 
+/* Replace the model data (tree / series) with new data of the SAME shape
+ * (host pointer; copied to the device on the handle's stream); parameters
+ * are kept.  With smc_reset this runs a new sweep without re-creating the
+ * handle (the per-step input upload of bench.py's e2e figure). */
+int smc_set_data(smc_handle h, const double* data, uint64_t data_len);
+
 /* Re-initialise for a fresh sweep: pc = b0, log Z = 0, epoch = 0, new seed. */
 int smc_reset(smc_handle h, uint64_t seed);
 

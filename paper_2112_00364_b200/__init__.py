@@ -82,6 +82,7 @@ _sig = {
     "smc_reset": ([H, C.c_uint64], C.c_int),
     "smc_set_timing": ([H, C.c_int32], C.c_int),
     "smc_set_graph": ([H, C.c_int32], C.c_int),
+    "smc_set_data": ([H, C.POINTER(C.c_double), C.c_uint64], C.c_int),
     "smc_run": ([H], C.c_int),
     "smc_step": ([H, C.POINTER(C.c_int32)], C.c_int),
     "smc_log_z": ([H], C.c_double),
@@ -224,6 +225,11 @@ class Smc:
     def set_stream(self, stream):
         """stream: torch.cuda.Stream, raw cudaStream_t int, or None."""
         _check(self.h, _lib.smc_set_stream(self.h, C.c_void_p(_stream_ptr(stream))))
+
+    def set_data(self, data):
+        d = np.ascontiguousarray(data, dtype=np.float64)
+        self._data_keep = d
+        _check(self.h, _lib.smc_set_data(self.h, _dptr(d), d.size))
 
     def set_graph(self, on=True):
         _check(self.h, _lib.smc_set_graph(self.h, 1 if on else 0))

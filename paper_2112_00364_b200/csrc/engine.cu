@@ -865,6 +865,41 @@ int smc_set_stream(smc_handle h, void* s) {
   return SMC_OK;
 }
 
+int smc_set_data(smc_handle h, const double* data, uint64_t data_len) {
+  if (!h) return fail(h, SMC_EINVAL, "NULL handle");
+  if (h->kind == SMC_RESAMPLE_BENCH || h->kind == SMC_GEOMETRIC || h->kind == SMC_CONSTW)
+    return fail(h, SMC_ESTATE, "model has no data");
+  // rebuild the device table exactly as setup_model does, same shape required
+  smc_model m{};
+  m.kind = h->kind;
+  m.data = data;
+  m.data_len = data_len;
+  m.flags = h->flags;
+  std::vector<double> old = h->h_table;
+  const int old_n = h->mc.n;
+  double saved_p[12];
+  std::memcpy(saved_p, h->mc.p, sizeof(saved_p));
+  std::vector<double> prm(saved_p, saved_p + 12);
+  m.params = prm.data();
+  m.n_params = 0;                       // keep the handle's parameters
+  h->h_table.clear();
+  int rc = setup_model(h, &m);
+  const double derived_p5 = h->mc.p[5];          // ClaDS2: root child order of the NEW tree
+  std::memcpy(h->mc.p, saved_p, sizeof(saved_p));
+  if (h->kind == SMC_CLADS2) h->mc.p[5] = derived_p5;
+  if (rc == SMC_OK && (h->mc.n != old_n || h->h_table.size() != old.size()))
+    rc = fail(h, SMC_EINVAL, "new data must have the same shape");
+  if (rc != SMC_OK) {
+    h->h_table = old;
+    h->mc.n = old_n;
+    return rc;
+  }
+  h->mc.table = h->d_table;
+  CU(cudaMemcpyAsync(h->d_table, h->h_table.data(), h->h_table.size() * sizeof(double),
+                     cudaMemcpyHostToDevice, h->stream));
+  return SMC_OK;
+}
+
 int smc_set_graph(smc_handle h, int32_t on) {
   if (!h) return fail(h, SMC_EINVAL, "NULL handle");
   h->use_graph = on != 0;

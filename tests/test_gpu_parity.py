@@ -331,3 +331,35 @@ def test_resample_step_sharded(smc, shards):
         np.testing.assert_array_equal(h.ancestors(), ref["anc"])
         assert h.distinct() == len(np.unique(ref["anc"]))
     np.testing.assert_array_equal(_aos_shards(smc, h.state(), shards, S), ref_st)
+
+
+@pytest.mark.parametrize("lineage", [False, True])
+def test_set_data_matches_fresh_handle(smc, lineage):
+    t5 = inputs.tree("tree5")
+    t5b = dict(t5)
+    t5b["age"] = [a * 1.3 for a in t5["age"]]                 # same shape, other ages
+    h = smc.Smc(smc.Model.crbd(t5, lineage=lineage), 2000, 5)
+    h.run()
+    h.set_data(smc.tree_data(t5b))
+    h.reset(6)
+    h.run()
+    ref = smc.Smc(smc.Model.crbd(t5b, lineage=lineage), 2000, 6)
+    ref.run()
+    assert h.log_z == ref.log_z
+    np.testing.assert_array_equal(h.log_weights(), ref.log_weights())
+    with pytest.raises(smc.SmcError):
+        h.set_data(smc.tree_data(inputs.tree("tree90")))     # different shape
+
+
+def test_set_data_seir(smc):
+    y = inputs.seir_series()
+    y2 = np.maximum(y - 1.0, 0.0)                           # same length, other observations
+    h = smc.Smc(smc.Model.seir(y), 1500, 9)
+    assert h.run_status() in (smc.OK, smc.EREJECTED)
+    h.set_data(y2)
+    h.reset(10)
+    rc = h.run_status()
+    ref = smc.Smc(smc.Model.seir(y2), 1500, 10)
+    assert rc == ref.run_status()
+    assert h.log_z == ref.log_z
+    np.testing.assert_array_equal(h.log_weights(), ref.log_weights())
