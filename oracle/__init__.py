@@ -65,6 +65,10 @@ def lib():
             L.oracle_smc_create.restype = vp
             L.oracle_smc_step.argtypes = [vp, P(i32)]
             L.oracle_smc_run.argtypes = [vp]
+            L.oracle_smc_set_ess.argtypes = [vp, u32, u32]
+            L.oracle_smc_last_ess.argtypes = [vp]
+            L.oracle_smc_last_ess.restype = d
+            L.oracle_ess_gate.argtypes = [P(d), u64, u32, u32, P(d)]
             L.oracle_smc_log_z.argtypes = [vp]
             L.oracle_smc_log_z.restype = d
             L.oracle_smc_epoch.argtypes = [vp]
@@ -163,6 +167,16 @@ def systematic(q, z):
     return anc
 
 
+def ess_gate(lw, a, b):
+    """(resample?, ESS) for log-weights lw and threshold a/b (exact gate)."""
+    lw = np.ascontiguousarray(lw, dtype=np.float64)
+    e = C.c_double()
+    rc = lib().oracle_ess_gate(_p(lw, C.c_double), lw.size, a, b, C.byref(e))
+    if rc < 0:
+        raise OracleError(-rc)
+    return bool(rc), e.value
+
+
 def quantize(lw):
     lw = np.ascontiguousarray(lw, dtype=np.float64)
     q = np.zeros(lw.size, dtype=np.uint64)
@@ -217,6 +231,16 @@ class Smc:
 
     def run(self):
         return lib().oracle_smc_run(self.h)
+
+    def set_ess(self, a, b):
+        """ESS threshold tau = a / b (a >= b: resample at every checkpoint)."""
+        rc = lib().oracle_smc_set_ess(self.h, a, b)
+        if rc:
+            raise OracleError(rc)
+
+    @property
+    def last_ess(self):
+        return lib().oracle_smc_last_ess(self.h)
 
     @property
     def log_z(self):

@@ -864,6 +864,52 @@ void systematic(const std::vector<uint64_t>& q, uint64_t N, u128 W, uint64_t z, 
   }
 }
 
+// ESS-adaptive resampling: with
+// integer weights q, ESS = W^2 / sum q^2.  Resample iff tau >= 1 or
+// ESS < tau N, tau = a/b, evaluated exactly:  b W^2 < a N sum q^2.
+struct U512 { uint64_t w[8]; };
+U512 add_mul(U512 acc, u128 x, u128 y) {            // acc += x * y
+  U256 p = mul128(x, y);
+  uint64_t carry = 0;
+  for (int i = 0; i < 8; ++i) {
+    uint64_t add = i < 4 ? ((uint64_t)p.w[2 * i] | ((uint64_t)p.w[2 * i + 1] << 32)) : 0;
+    u128 cur = (u128)acc.w[i] + add + carry;
+    acc.w[i] = (uint64_t)cur;
+    carry = (uint64_t)(cur >> 64);
+  }
+  return acc;
+}
+U512 mul_small(U512 a, uint64_t m) {
+  U512 r{};
+  u128 carry = 0;
+  for (int i = 0; i < 8; ++i) {
+    u128 cur = (u128)a.w[i] * m + carry;
+    r.w[i] = (uint64_t)cur;
+    carry = cur >> 64;
+  }
+  return r;
+}
+bool less512(const U512& a, const U512& b) {
+  for (int i = 7; i >= 0; --i) if (a.w[i] != b.w[i]) return a.w[i] < b.w[i];
+  return false;
+}
+bool ess_resample(const std::vector<uint64_t>& q, u128 W, uint64_t N, uint32_t a, uint32_t b) {
+  if (a >= b) return true;                                 // tau >= 1: always (plain Alg. 1)
+  U512 Q2{};
+  for (uint64_t k = 0; k < q.size(); ++k) Q2 = add_mul(Q2, q[k], q[k]);
+  U512 W2{};
+  W2 = add_mul(W2, W, W);
+  U512 lhs = mul_small(W2, b);
+  U512 rhs = mul_small(mul_small(Q2, a), N);
+  return less512(lhs, rhs);
+}
+double ess_value(const std::vector<uint64_t>& q, u128 W) {  // diagnostics only
+  long double s2 = 0;
+  for (uint64_t v : q) s2 += (long double)v * (long double)v;
+  long double w = (long double)W;
+  return s2 > 0 ? (double)(w * w / s2) : 0.0;
+}
+
 // ----------------------------------------------------------------------------
 // Algorithm 1 with the RootPPL loop order:
 // propagate all particles to their next checkpoint; stop if all reached
@@ -880,6 +926,8 @@ struct SmcBase {
   int status = E_OK;
   bool finished = false;
   uint64_t draws = 0, overflow = 0, resamples = 0, alive_steps = 0;
+  uint32_t ess_a = 1, ess_b = 1;        // tau = a / b (>= 1: resample at every checkpoint)
+  double last_ess = 0.0;
   std::vector<double> lw;
   std::vector<uint32_t> anc;
   std::vector<uint64_t> last_q;
@@ -922,9 +970,9 @@ struct Smc : SmcBase {
   }
   int step(int* done) override {
     if (finished || status != E_OK) { *done = 1; return status; }
-    // Propagation (Alg. 1 step 2)
+    // Propagation (Alg. 1 step 2).  lw holds the weight
+    // accumulated since the last resample (reset to 0 right after it).
     for (uint64_t n = 0; n < N; ++n) {
-      lw[n] = 0.0;
       if (st[n].pc == PC_STOP) continue;      // b_stop self-loop
       ++alive_steps;
       Stream rs = make_stream(seed, (uint32_t)n, t, TAG_PARTICLE, &draws);
@@ -943,14 +991,24 @@ struct Smc : SmcBase {
       finished = true; *done = 1;
       return rc;
     }
+    if (!alive) {
+      logz += last.logz_inc;
+      finished = true; *done = 1; return E_OK;
+    }
+    last_ess = ess_value(last_q, last.W);
+    if (!ess_resample(last_q, last.W, N, ess_a, ess_b)) {      // ESS gate (R-19)
+      ++t;
+      *done = 0;
+      return E_OK;                                             // weights carried over
+    }
     logz += last.logz_inc;
-    if (!alive) { finished = true; *done = 1; return E_OK; }
     // Resampling (Alg. 1 step 3; systematic)
     last.z = resample_z(seed, t);
     systematic(last_q, N, last.W, last.z, anc.data());
     tmp.resize(N);
     for (uint64_t j = 0; j < N; ++j) tmp[j] = st[anc[j]];
     st.swap(tmp);
+    for (uint64_t n = 0; n < N; ++n) lw[n] = 0.0;
     ++resamples;
     ++t;
     *done = 0;
@@ -1169,6 +1227,22 @@ void* oracle_smc_create(int kind, const double* data, uint64_t data_len,
 }
 
 int oracle_smc_step(void* h, int* done) { return ((SmcBase*)h)->step(done); }
+// ESS threshold tau = a / b (R-19); a >= b: resample at every checkpoint.
+int oracle_smc_set_ess(void* h, uint32_t a, uint32_t b) {
+  if (b == 0) return E_INVAL;
+  ((SmcBase*)h)->ess_a = a; ((SmcBase*)h)->ess_b = b;
+  return E_OK;
+}
+double oracle_smc_last_ess(void* h) { return ((SmcBase*)h)->last_ess; }
+// Exact ESS gate on caller weights (tests): 1 = resample.
+int oracle_ess_gate(const double* lw, uint64_t N, uint32_t a, uint32_t b, double* ess) {
+  std::vector<uint64_t> q;
+  ResampleOut o{};
+  int rc = normalise(lw, N, q, o);
+  if (rc != E_OK) return -rc;
+  if (ess) *ess = ess_value(q, o.W);
+  return ess_resample(q, o.W, N, a, b) ? 1 : 0;
+}
 int oracle_smc_run(void* h) {
   int done = 0, rc = 0;
   while (!done) { rc = oracle_smc_step(h, &done); }
