@@ -222,6 +222,8 @@ def bench_sweeps(args, wl, smc, torch, world, rank):
     else:
         from paper_2112_00364_b200 import dist as sdist
         h = sdist.sharded(model, N, seed=1, stream=stream)
+    ea, eb = (int(x) for x in args.ess.split("/"))
+    h.set_ess_threshold(ea, eb)
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda")
     # warm-up sweeps (untimed; the first also captures the whole-run CUDA graph)
     for w in range(args.warmup):
@@ -262,6 +264,7 @@ def bench_sweeps(args, wl, smc, torch, world, rank):
     h.set_timing(True)
     prop_ms = res_ms = 0.0
     res_bytes = 0
+    n_resamples = 0
     for k in range(args.steps):
         h.reset(1 + k)
         h.run()
@@ -273,12 +276,13 @@ def bench_sweeps(args, wl, smc, torch, world, rank):
         # algorithmic resample bytes of the sweep: per resample N*20 + S*(D + N),
         # plus the final epoch's reduce (8 B/particle)
         res_bytes += st["resamples"] * n_loc * (20 + sb) + sb * st["distinct"] + 8 * n_loc
+        n_resamples += st["resamples"]
     h.set_timing(False)
     # graph body = 2 epochs x (propagate, reduce, anc_gather, finalize) + set_condition
     E = steps_done // args.steps
     launches = args.steps * 9 * ((E + 1) // 2)
     return dict(h=h, model=model, N=N, t_ms=t_ms, value=value, sweeps=sweeps_per_s, prop_ms=prop_ms,
-                res_bytes=res_bytes,
+                res_bytes=res_bytes, resamples_per_sweep=n_resamples / args.steps,
                 res_ms=res_ms, draws=draws, alive_steps=alive_steps, epochs=steps_done,
                 launches=launches, clocks=clk.summary(torch.cuda.current_device()),
                 logz=float(np.mean(logzs)))
@@ -483,9 +487,11 @@ def run_ours(args, wl):
                 vs_baseline=None, dtype="f64", data="synthetic",
                 config=dict(workload=args.workload, desc=wl["desc"], n_per_gpu=N,
                             rng=args.rng if wl["model"] in ("crbd", "clads2") else "sequential",
+                            ess_threshold=args.ess,
                             epochs_per_sweep=r["epochs"] // args.steps,
                             l2="flushed between steps (state fits L2 within a sweep)"),
                 sweeps_per_s=r["sweeps"], mean_log_z=r["logz"],
+                resamples_per_sweep=r["resamples_per_sweep"],
                 phase_ms=dict(propagate=r["prop_ms"] / args.steps, resample=r["res_ms"] / args.steps,
                               propagate_share=prop_frac),
                 draws_per_particle_step=r["draws"] / max(r["alive_steps"], 1),
@@ -530,6 +536,8 @@ def main():
     ap.add_argument("--rng", default="lineage", choices=sorted(RNG),
                     help="tree models: lineage-keyed side trees (DESIGN R-18, cooperative kernel) "
                          "or the sequential per-particle stream (R-11)")
+    ap.add_argument("--ess", default="1/1",
+                    help="ESS-adaptive resampling threshold a/b (DESIGN R-19); 1/1 = every checkpoint")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)

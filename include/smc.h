@@ -176,6 +176,14 @@ int smc_set_stream(smc_handle h, void* cuda_stream);
 
 /* --- running ---------------------------------------------------------------- */
 
+/* ESS-adaptive resampling: resample at a
+ * checkpoint only if ESS < tau N, tau = a / b, decided exactly in integers
+ * (b W^2 < a N sum q^2); otherwise weights accumulate and log Z is not
+ * updated until the next resample or the end.  a >= b (default 1/1):
+ * resample at every checkpoint (plain Algorithm 1).  Persists across
+ * smc_reset. */
+int smc_set_ess_threshold(smc_handle h, uint32_t a, uint32_t b);
+
 /* smc_run as ONE CUDA graph launch (default on): a WHILE conditional node
  * repeats {epoch, epoch} until the device sets done; no host round trip per
  * epoch.  Off: a host loop of smc_step (needed with a host all-gather comm or

@@ -928,6 +928,7 @@ struct SmcBase {
   uint64_t draws = 0, overflow = 0, resamples = 0, alive_steps = 0;
   uint32_t ess_a = 1, ess_b = 1;        // tau = a / b (>= 1: resample at every checkpoint)
   double last_ess = 0.0;
+  bool carry = false;                   // last checkpoint did not resample: lw accumulates
   std::vector<double> lw;
   std::vector<uint32_t> anc;
   std::vector<uint64_t> last_q;
@@ -971,8 +972,10 @@ struct Smc : SmcBase {
   int step(int* done) override {
     if (finished || status != E_OK) { *done = 1; return status; }
     // Propagation (Alg. 1 step 2).  lw holds the weight
-    // accumulated since the last resample (reset to 0 right after it).
+    // accumulated since the last resample: it restarts at 0 unless the last
+    // checkpoint skipped resampling (R-19).
     for (uint64_t n = 0; n < N; ++n) {
+      if (!carry) lw[n] = 0.0;
       if (st[n].pc == PC_STOP) continue;      // b_stop self-loop
       ++alive_steps;
       Stream rs = make_stream(seed, (uint32_t)n, t, TAG_PARTICLE, &draws);
@@ -997,10 +1000,12 @@ struct Smc : SmcBase {
     }
     last_ess = ess_value(last_q, last.W);
     if (!ess_resample(last_q, last.W, N, ess_a, ess_b)) {      // ESS gate (R-19)
+      carry = true;                                            // weights carried over
       ++t;
       *done = 0;
-      return E_OK;                                             // weights carried over
+      return E_OK;
     }
+    carry = false;
     logz += last.logz_inc;
     // Resampling (Alg. 1 step 3; systematic)
     last.z = resample_z(seed, t);
@@ -1008,7 +1013,6 @@ struct Smc : SmcBase {
     tmp.resize(N);
     for (uint64_t j = 0; j < N; ++j) tmp[j] = st[anc[j]];
     st.swap(tmp);
-    for (uint64_t n = 0; n < N; ++n) lw[n] = 0.0;
     ++resamples;
     ++t;
     *done = 0;

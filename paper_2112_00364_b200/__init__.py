@@ -82,6 +82,7 @@ _sig = {
     "smc_reset": ([H, C.c_uint64], C.c_int),
     "smc_set_timing": ([H, C.c_int32], C.c_int),
     "smc_set_graph": ([H, C.c_int32], C.c_int),
+    "smc_set_ess_threshold": ([H, C.c_uint32, C.c_uint32], C.c_int),
     "smc_set_data": ([H, C.POINTER(C.c_double), C.c_uint64], C.c_int),
     "smc_run": ([H], C.c_int),
     "smc_step": ([H, C.POINTER(C.c_int32)], C.c_int),
@@ -230,6 +231,10 @@ class Smc:
         d = np.ascontiguousarray(data, dtype=np.float64)
         self._data_keep = d
         _check(self.h, _lib.smc_set_data(self.h, _dptr(d), d.size))
+
+    def set_ess_threshold(self, a, b):
+        """Resample only when ESS < (a/b) N; a >= b: at every checkpoint."""
+        _check(self.h, _lib.smc_set_ess_threshold(self.h, int(a), int(b)))
 
     def set_graph(self, on=True):
         _check(self.h, _lib.smc_set_graph(self.h, 1 if on else 0))

@@ -70,6 +70,7 @@ struct Shard {
   double* lw = nullptr;
   u128* tile_sum = nullptr;
   u128* tile_excl = nullptr;
+  U192* tile_q2 = nullptr;
   Ctrl* ctrl = nullptr;
   uint4** d_dst_planes[2] = {nullptr, nullptr};  // device arrays [world]
   uint32_t** d_dst_anc = nullptr;                 // device array [world]
@@ -98,7 +99,8 @@ struct smc_ctx {
   std::vector<double> h_table;
   double* d_logfact = nullptr;    // SEIR: lgamma(k+1) table (model setup, host libm)
   RecA* d_recA = nullptr;         // [2][world]
-  u128* d_recB = nullptr;         // [2][world]
+  RecB* d_recB = nullptr;         // [2][world]
+  unsigned ess_a = 1, ess_b = 1;  // ESS threshold (R-19)
   int* d_barrier = nullptr;
   std::vector<Shard> shards;
   cudaStream_t stream = nullptr;
@@ -318,6 +320,7 @@ int alloc_shard(smc_ctx* h, Shard& s) {
   CU(cudaMalloc(&s.lw, n * sizeof(double)));
   CU(cudaMalloc(&s.tile_sum, (size_t)h->n_tiles * sizeof(u128)));
   CU(cudaMalloc(&s.tile_excl, (size_t)h->n_tiles * sizeof(u128)));
+  CU(cudaMalloc(&s.tile_q2, (size_t)h->n_tiles * sizeof(U192)));
   CU(cudaMalloc(&s.ctrl, sizeof(Ctrl)));
   CU(cudaMalloc(&s.d_dst_planes[0], h->world * sizeof(uint4*)));
   CU(cudaMalloc(&s.d_dst_planes[1], h->world * sizeof(uint4*)));
@@ -343,10 +346,12 @@ int reset_device(smc_ctx* h) {
   c.last_inc = 0.0;
   c.first_err = ~0ull;
   c.seed = h->seed;
+  c.ess_a = h->ess_a;
+  c.ess_b = h->ess_b;
   std::vector<RecA> ra(2 * h->world);
   for (auto& r : ra) { r.key = LLONG_MIN; r.alive = 0; r.flags = 0; }
   CU(cudaMemcpyAsync(h->d_recA, ra.data(), ra.size() * sizeof(RecA), cudaMemcpyHostToDevice, h->stream));
-  CU(cudaMemsetAsync(h->d_recB, 0, 2 * h->world * sizeof(u128), h->stream));
+  CU(cudaMemsetAsync(h->d_recB, 0, 2 * h->world * sizeof(RecB), h->stream));
   for (auto& s : h->shards) {
     CU(cudaMemcpyAsync(s.ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, h->stream));
     // pc = b0 = 0 and all fields zero; lw = 0; anc = identity
@@ -413,7 +418,7 @@ int common_init(smc_ctx* h, const smc_model* m, unsigned long long n_per, int wo
     h->mc.n_logfact = nlf;
   }
   CU(cudaMalloc(&h->d_recA, 2 * world * sizeof(RecA)));
-  CU(cudaMalloc(&h->d_recB, 2 * world * sizeof(u128)));
+  CU(cudaMalloc(&h->d_recB, 2 * world * sizeof(RecB)));
   CU(cudaMalloc(&h->d_barrier, sizeof(int)));
   CU(cudaMallocHost(&h->h_ctrl, sizeof(Ctrl)));
   if (h->lineage) {
@@ -539,6 +544,7 @@ ResArgs res_args(smc_ctx* h, Shard& s, const double* lw, const uint4* src, int d
   a.recB = h->d_recB;
   a.tile_sum = s.tile_sum;
   a.tile_excl = s.tile_excl;
+  a.tile_q2 = s.tile_q2;
   a.n_tiles = h->n_tiles;
   a.src_planes = src;
   a.planes = h->planes;
@@ -596,7 +602,7 @@ int enqueue_epoch(smc_ctx* h) {
     launch_reduce(h, res_args(h, s, s.lw, s.planes[cur], cur ^ 1));
   }
   CU(cudaGetLastError());
-  rc = allgather_rec(h, h->d_recB + cur * h->world, rec);
+  rc = allgather_rec(h, h->d_recB + cur * h->world, sizeof(RecB));
   if (rc) return rc;
   for (auto& s : h->shards) launch_anc_gather(h, res_args(h, s, s.lw, s.planes[cur], cur ^ 1));
   CU(cudaGetLastError());
@@ -835,7 +841,7 @@ void smc_destroy(smc_handle h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
   for (auto& s : h->shards) {
-    cudaFree(s.ipc_block); cudaFree(s.lw); cudaFree(s.tile_sum); cudaFree(s.tile_excl);
+    cudaFree(s.ipc_block); cudaFree(s.lw); cudaFree(s.tile_sum); cudaFree(s.tile_excl); cudaFree(s.tile_q2);
     cudaFree(s.ctrl); cudaFree(s.d_dst_planes[0]); cudaFree(s.d_dst_planes[1]); cudaFree(s.d_dst_anc);
   }
   cudaFree(h->d_table); cudaFree(h->d_logfact); cudaFree(h->d_recA); cudaFree(h->d_recB); cudaFree(h->d_barrier);
@@ -897,6 +903,18 @@ int smc_set_data(smc_handle h, const double* data, uint64_t data_len) {
   h->mc.table = h->d_table;
   CU(cudaMemcpyAsync(h->d_table, h->h_table.data(), h->h_table.size() * sizeof(double),
                      cudaMemcpyHostToDevice, h->stream));
+  return SMC_OK;
+}
+
+int smc_set_ess_threshold(smc_handle h, uint32_t a, uint32_t b) {
+  if (!h || b == 0) return fail(h, SMC_EINVAL, "threshold a/b needs b > 0");
+  h->ess_a = a;
+  h->ess_b = b;
+  for (auto& s : h->shards) {
+    CU(cudaMemcpyAsync(&s.ctrl->ess_a, &h->ess_a, sizeof(unsigned), cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemcpyAsync(&s.ctrl->ess_b, &h->ess_b, sizeof(unsigned), cudaMemcpyHostToDevice, h->stream));
+  }
+  CU(cudaStreamSynchronize(h->stream));
   return SMC_OK;
 }
 
@@ -989,7 +1007,9 @@ static int current_parity(smc_ctx* h) {
     return (int)(h->enq & 1);
   }
   if (read_ctrl(h)) return -1;
-  return (int)(h->h_ctrl->resamples & 1);
+  // every non-final epoch swaps buffers (resample or, under R-19, an identity
+  // copy) and advances ctrl->epoch; the final epoch does neither
+  return (int)(h->h_ctrl->epoch & 1);
 }
 
 int smc_state(smc_handle h, void* out, uint64_t bytes) {
@@ -1207,7 +1227,7 @@ int smc_resample_step(smc_handle h, uint32_t epoch) {
   int rc = allgather_rec(h, h->d_recA + par * h->world, 16);
   if (rc) return rc;
   for (auto& s : h->shards) launch_reduce(h, res_args(h, s, s.lw, s.planes[cur], cur ^ 1));
-  rc = allgather_rec(h, h->d_recB + par * h->world, 16);
+  rc = allgather_rec(h, h->d_recB + par * h->world, sizeof(RecB));
   if (rc) return rc;
   for (auto& s : h->shards) launch_anc_gather(h, res_args(h, s, s.lw, s.planes[cur], cur ^ 1));
   rc = barrier(h);

@@ -36,6 +36,14 @@ struct RecA {
   unsigned flags;      // bit 0: NaN or +inf log-weight seen
 };
 
+// Record all-gathered after the reduce pass (48 B per shard): integer total
+// weight W and, for ESS-adaptive resampling, sum of q^2 (192-bit).
+struct RecB {
+  u128 W;
+  unsigned long long q2[3];
+  unsigned long long pad;
+};
+
 struct Ctrl {
   double logz;
   double last_inc;
@@ -52,6 +60,8 @@ struct Ctrl {
   unsigned long long draws;          // uniforms drawn by propagation (all epochs)
   unsigned long long seed;           // Philox key of the run (device-resident: graphs survive reset)
   unsigned batch;                    // next 256-particle batch (persistent propagation grids)
+  unsigned ess_a, ess_b;             // ESS threshold tau = a / b (a >= b: always resample, R-19)
+  unsigned carry;                    // 1: the last checkpoint did not resample, lw accumulates
   unsigned max_rounds;               // diag: longest cooperative phase (rounds) in a batch
   unsigned long long side_roots;     // diag: hidden events (side-tree roots) generated
   unsigned max_side_nodes;           // diag: largest per-particle side-tree node count
@@ -115,6 +125,61 @@ __device__ __forceinline__ bool lt_u256(const U256& a, const U256& b) {
 #pragma unroll
   for (int i = 3; i >= 0; --i)
     if (a.w[i] != b.w[i]) return a.w[i] < b.w[i];
+  return false;
+}
+
+// 192-bit accumulation of q^2 (q < 2^62+1, N < 2^32: sum < 2^157).
+struct U192 { unsigned long long w[3]; };
+__device__ __forceinline__ void add_u192(U192& a, const U192& b) {
+  const u128 s0 = (u128)a.w[0] + b.w[0];
+  const u128 s1 = (u128)a.w[1] + b.w[1] + (unsigned long long)(s0 >> 64);
+  a.w[0] = (unsigned long long)s0;
+  a.w[1] = (unsigned long long)s1;
+  a.w[2] = a.w[2] + b.w[2] + (unsigned long long)(s1 >> 64);
+}
+__device__ __forceinline__ void add_u192_u128(U192& a, u128 b) {
+  U192 t;
+  t.w[0] = (unsigned long long)b; t.w[1] = (unsigned long long)(b >> 64); t.w[2] = 0;
+  add_u192(a, t);
+}
+__device__ __forceinline__ U192 shfl_xor_u192(const U192& v, int d) {
+  U192 r;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) r.w[i] = __shfl_xor_sync(0xffffffffu, v.w[i], d);
+  return r;
+}
+// 4-limb (256-bit) product x * m.
+__device__ __forceinline__ void mul_limbs(const unsigned long long* x, int n, unsigned long long m,
+                                          unsigned long long* out /*[4]*/) {
+  u128 carry = 0;
+  for (int i = 0; i < 4; ++i) {
+    const u128 cur = (i < n ? (u128)x[i] * m : 0) + carry;
+    out[i] = (unsigned long long)cur;
+    carry = cur >> 64;
+  }
+}
+// ESS gate (R-19): resample iff tau >= 1 or b W^2 < a N sum q^2, exactly.
+__device__ __forceinline__ bool ess_resample(u128 W, const U192& Q2, unsigned long long N,
+                                             unsigned a, unsigned b) {
+  if (a >= b) return true;
+  const unsigned long long w[2] = {(unsigned long long)W, (unsigned long long)(W >> 64)};
+  unsigned long long W2[4] = {0, 0, 0, 0};
+  {   // W^2 (< 2^190)
+    const u128 p00 = (u128)w[0] * w[0], p01 = (u128)w[0] * w[1], p11 = (u128)w[1] * w[1];
+    W2[0] = (unsigned long long)p00;
+    const u128 mid = (p00 >> 64) + 2 * (u128)(unsigned long long)p01;
+    W2[1] = (unsigned long long)mid;
+    const u128 hi = (mid >> 64) + 2 * (p01 >> 64) + (unsigned long long)p11;
+    W2[2] = (unsigned long long)hi;
+    W2[3] = (unsigned long long)(hi >> 64) + (unsigned long long)(p11 >> 64);
+  }
+  unsigned long long lhs[4], t[4], rhs[4];
+  mul_limbs(W2, 4, b, lhs);
+  mul_limbs(Q2.w, 3, a, t);
+  mul_limbs(t, 4, N, rhs);
+#pragma unroll
+  for (int i = 3; i >= 0; --i)
+    if (lhs[i] != rhs[i]) return lhs[i] < rhs[i];
   return false;
 }
 
@@ -203,7 +268,8 @@ __global__ void __launch_bounds__(kThreads, M::kMinBlocks) propagate_kernel(Prop
   const unsigned epoch = a.ctrl->epoch;
   const unsigned long long i = (unsigned long long)blockIdx.x * kThreads + threadIdx.x;
   const bool valid = i < a.n_local;
-  double lw = 0.0;
+  const bool carry = a.ctrl->carry != 0;               // R-19: no resample at the last checkpoint
+  double lw = (valid && carry) ? a.lw[i] : 0.0;
   int start_alive = 0, end_alive = 0;
   bool bad = false;
   unsigned long long drw = 0;
@@ -279,7 +345,8 @@ struct ResArgs {
   unsigned long long n_total;
   int world, rank;
   RecA* recA;                         // [2][world]
-  u128* recB;                         // [2][world] shard totals
+  RecB* recB;                         // [2][world] shard totals (W, sum q^2)
+  U192* tile_q2;                      // [n_tiles] (ESS only)
   u128* tile_sum;                     // [n_tiles]
   u128* tile_excl;                    // [n_tiles]
   int n_tiles;
@@ -321,9 +388,11 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(ResArgs a) {
   constexpr int kItems = ITEMS;
   constexpr int kTPB = 2;                               // tiles per CTA
   __shared__ u128 s_w[kTPB][kThreads / 32];
+  __shared__ U192 s_q2[kTPB][kThreads / 32];
   __shared__ unsigned s_ticket;
   if (*(volatile unsigned*)&a.ctrl->done) return;
   const unsigned par = a.ctrl->epoch & 1;
+  const bool ess = a.ctrl->ess_a < a.ctrl->ess_b;         // uniform
   const Global G = read_global(a.recA + par * a.world, a.world);
   if (!G.ok) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -349,12 +418,23 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(ResArgs a) {
   }
 #pragma unroll
   for (int tt = 0; tt < kTPB; ++tt) {
-    u128 acc = 0;
+    u128 acc = 0, acc2 = 0;                              // acc2: sum of q^2 (< 8 * 2^124)
 #pragma unroll
-    for (int r = 0; r < kItems; ++r) acc += quantize(v[tt][r], G.m);
+    for (int r = 0; r < kItems; ++r) {
+      const unsigned long long q = quantize(v[tt][r], G.m);
+      acc += q;
+      if (ess) acc2 += (u128)q * q;
+    }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) acc += shfl_xor_u128(acc, d);
     if (lane == 0) s_w[tt][warp] = acc;
+    if (ess) {
+      U192 q2;
+      q2.w[0] = (unsigned long long)acc2; q2.w[1] = (unsigned long long)(acc2 >> 64); q2.w[2] = 0;
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) add_u192(q2, shfl_xor_u192(q2, d));
+      if (lane == 0) s_q2[tt][warp] = q2;
+    }
   }
   __syncthreads();
   if (threadIdx.x < kTPB) {
@@ -363,6 +443,11 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(ResArgs a) {
       u128 t = 0;
       for (int w = 0; w < kThreads / 32; ++w) t += s_w[threadIdx.x][w];
       a.tile_sum[tile] = t;
+      if (ess) {
+        U192 q = s_q2[threadIdx.x][0];
+        for (int w = 1; w < kThreads / 32; ++w) add_u192(q, s_q2[threadIdx.x][w]);
+        a.tile_q2[tile] = q;
+      }
     }
   }
   if (threadIdx.x == 0) {
@@ -396,21 +481,41 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(ResArgs a) {
     run += ld_cg_u128(a.tile_sum + t);
   }
   if (threadIdx.x == kThreads - 1) {
-    a.recB[par * a.world + a.rank] = run;     // shard total
+    a.recB[par * a.world + a.rank].W = run;     // shard total
     a.ctrl->counter = 0;
+  }
+  if (ess && threadIdx.x == 0) {
+    U192 q = {{0, 0, 0}};
+    for (int t = 0; t < nt; ++t) {
+      U192 v;
+      const unsigned long long* src = (const unsigned long long*)(a.tile_q2 + t);
+      v.w[0] = __ldcg(src); v.w[1] = __ldcg(src + 1); v.w[2] = __ldcg(src + 2);
+      add_u192(q, v);
+    }
+    RecB* rb = a.recB + par * a.world + a.rank;
+    rb->q2[0] = q.w[0]; rb->q2[1] = q.w[1]; rb->q2[2] = q.w[2];
   }
 }
 
 // ============================================================================
 // anc_gather: ancestors of the tile's output slots + fused state gather
 // ============================================================================
-__device__ __forceinline__ Grid make_grid(const ResArgs& a, const u128* B, unsigned epoch,
+__device__ __forceinline__ U192 total_q2(const RecB* B, int world) {
+  U192 q = {{0, 0, 0}};
+  for (int g = 0; g < world; ++g) {
+    U192 v;
+    v.w[0] = B[g].q2[0]; v.w[1] = B[g].q2[1]; v.w[2] = B[g].q2[2];
+    add_u192(q, v);
+  }
+  return q;
+}
+__device__ __forceinline__ Grid make_grid(const ResArgs& a, const RecB* B, unsigned epoch,
                                           u128& prefix) {
   u128 W = 0;
   prefix = 0;
   for (int g = 0; g < a.world; ++g) {
-    if (g < a.rank) prefix += B[g];
-    W += B[g];
+    if (g < a.rank) prefix += B[g].W;
+    W += B[g].W;
   }
   const unsigned long long seed = a.ctrl->seed;
   const uint4 r = philox4x32_10(make_uint4(0u, epoch, 0u, 1u), (uint32_t)seed, (uint32_t)(seed >> 32));
@@ -441,9 +546,20 @@ __global__ void __launch_bounds__(kThreads) anc_gather_kernel(ResArgs a) {
   if (!G.ok || G.alive == 0) return;       // error, or final epoch: no resample
   u128 prefix;
   const Grid gr = make_grid(a, a.recB + par * a.world, epoch, prefix);
-
   const unsigned long long base = (unsigned long long)blockIdx.x * kTile;
   const int cnt = (int)min((unsigned long long)kTile, a.n_local - base);
+  if (!ess_resample(gr.W, total_q2(a.recB + par * a.world, a.world), a.n_total, a.ctrl->ess_a,
+                    a.ctrl->ess_b)) {
+    // ESS high enough: no resample (R-19); keep the states (copy to the other
+    // buffer so the epoch's buffer parity holds), ancestors unchanged
+    uint4* dst = a.dst_planes[a.rank];
+    const int np = P > 0 ? P : a.planes;
+    for (int k = threadIdx.x; k < cnt; k += kThreads)
+      for (int p = 0; p < np; ++p)
+        dst[(unsigned long long)p * a.n_local + base + k] =
+            __ldg(a.src_planes + (unsigned long long)p * a.n_local + base + k);
+    return;
+  }
   // striped (coalesced) load, blocked use
 #pragma unroll
   for (int r = 0; r < kItems; ++r) {
@@ -528,7 +644,7 @@ __global__ void __launch_bounds__(kThreads) anc_gather_kernel(ResArgs a) {
 // ============================================================================
 struct FinArgs {
   RecA* recA;
-  u128* recB;
+  RecB* recB;
   int world, rank;
   unsigned long long n_total;
   int strict;
@@ -552,19 +668,26 @@ __global__ void finalize_kernel(FinArgs a) {
     c->epochs = c->epochs + 1;
   } else {
     u128 W = 0;
-    for (int g = 0; g < a.world; ++g) W += a.recB[par * a.world + g];
+    for (int g = 0; g < a.world; ++g) W += a.recB[par * a.world + g].W;
     const double lwd = log(u128_trunc_double(W));
     const double inc = G.m + ((lwd - 62.0 * kLn2) - log((double)a.n_total));
     c->last_inc = inc;
-    c->logz = c->logz + inc;
     c->epochs = c->epochs + 1;
     if (a.strict && c->overflow) {
+      c->logz = c->logz + inc;
       c->status = ST_OVERFLOW;
       c->done = 1;
     } else if (G.alive == 0) {
+      c->logz = c->logz + inc;                         // final: no resample (R-6)
       c->done = 1;
-    } else {
+    } else if (ess_resample(W, total_q2(a.recB + par * a.world, a.world), a.n_total, c->ess_a,
+                            c->ess_b)) {
+      c->logz = c->logz + inc;
       c->resamples = c->resamples + 1;
+      c->carry = 0;
+      c->epoch = epoch + 1;
+    } else {
+      c->carry = 1;                                    // weights accumulate (R-19)
       c->epoch = epoch + 1;
     }
   }
@@ -574,7 +697,9 @@ __global__ void finalize_kernel(FinArgs a) {
   nx->key = LLONG_MIN;
   nx->alive = 0;
   nx->flags = 0;
-  a.recB[(par ^ 1) * a.world + a.rank] = 0;
+  RecB* nb = a.recB + (par ^ 1) * a.world + a.rank;
+  nb->W = 0;
+  nb->q2[0] = nb->q2[1] = nb->q2[2] = 0;
 }
 
 // ============================================================================
@@ -592,7 +717,7 @@ __global__ void set_condition_kernel(cudaGraphConditionalHandle hdl, const Ctrl*
 // resampler-only helpers (BASELINE configs[4])
 // ============================================================================
 // Set the epoch and clear the records of a standalone resampling step.
-__global__ void prep_resample_kernel(Ctrl* c, RecA* recA, u128* recB, int world, int rank,
+__global__ void prep_resample_kernel(Ctrl* c, RecA* recA, RecB* recB, int world, int rank,
                                      unsigned epoch) {
   if (threadIdx.x != 0) return;
   c->epoch = epoch;
@@ -603,7 +728,11 @@ __global__ void prep_resample_kernel(Ctrl* c, RecA* recA, u128* recB, int world,
   r->key = LLONG_MIN;
   r->alive = 1;          // a standalone step always resamples
   r->flags = 0;
-  recB[(epoch & 1) * world + rank] = 0;
+  RecB* b = recB + (epoch & 1) * world + rank;
+  b->W = 0;
+  b->q2[0] = b->q2[1] = b->q2[2] = 0;
+  c->ess_a = 1;              // a standalone step always resamples
+  c->ess_b = 1;
 }
 // Max of lw (the propagation epilogue's job in a full SMC run).
 __global__ void __launch_bounds__(kThreads) max_kernel(const double* lw, unsigned long long n,

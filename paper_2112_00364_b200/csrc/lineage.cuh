@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
     const uint32_t n_glob = (uint32_t)(p.shard_base + i);
     // ---------------- phase 1: the particle's own stream
     typename M::State st;
-    double lw = 0.0;
+    double lw = (valid && p.ctrl->carry) ? p.lw[i] : 0.0;   // R-19 carried weights
     int K = 0;
     bool active = false;
     if (valid) {

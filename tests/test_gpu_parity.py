@@ -363,3 +363,48 @@ def test_set_data_seir(smc):
     assert rc == ref.run_status()
     assert h.log_z == ref.log_z
     np.testing.assert_array_equal(h.log_weights(), ref.log_weights())
+
+
+# ------------------------------------------------------------- ESS-adaptive resampling (R-19)
+def run_pair_ess(smc, kind, data, params, N, seed, a, b, per_epoch=True, shards=1):
+    g, o = both(smc, kind, data, params, N, seed, shards)
+    g.set_ess_threshold(a, b)
+    o.set_ess(a, b)
+    while True:
+        rg, dg = g.step()
+        ro, do = o.step()
+        assert rg == ro and dg == do
+        if per_epoch or dg:
+            compare(g, o)
+        if dg:
+            break
+    if math.isfinite(o.log_z):
+        assert g.log_z == pytest.approx(o.log_z, rel=RTOL)
+    assert g.stats()["resamples"] == o.stats()["resamples"]
+    return g, o
+
+
+@pytest.mark.parametrize("a,b", [(1, 2), (0, 1), (9, 10)])
+@pytest.mark.parametrize("ck", [oracle.CRBD, oracle.CRBD_LR], ids=["seq", "lineage"])
+def test_ess_crbd(smc, ck, a, b):
+    run_pair_ess(smc, ck, inputs.tree("tree5"), [1.0, 0.3, 0.1], 3000, 5, a, b)
+
+
+@pytest.mark.parametrize("a,b", [(1, 2), (3, 4)])
+def test_ess_other_models(smc, a, b):
+    run_pair_ess(smc, oracle.GEOMETRIC, None, inputs.GEOMETRIC_PARAMS, 2500, 6, a, b)
+    run_pair_ess(smc, oracle.SSM, inputs.ssm_series(50), inputs.SSM_PARAMS, 2000, 7, a, b)
+    run_pair_ess(smc, oracle.CLADS2_LR, inputs.tree("tree90"), inputs.CLADS2_PARAMS, 2000, 8, a, b,
+                 per_epoch=False)
+
+
+def test_ess_virtual_shards_and_graph(smc):
+    run_pair_ess(smc, oracle.CRBD_LR, inputs.tree("tree90"), inputs.CRBD_PARAMS, 3 * 2000, 9, 1, 2,
+                 per_epoch=False, shards=3)
+    g, o = both(smc, oracle.CRBD_LR, inputs.tree("tree90"), inputs.CRBD_PARAMS, 4000, 10)
+    g.set_ess_threshold(1, 2)
+    o.set_ess(1, 2)
+    assert g.run_status() == o.run() == 0                  # whole-run graph
+    assert g.log_z == pytest.approx(o.log_z, rel=RTOL)
+    compare(g, o)
+    assert g.stats()["resamples"] == o.stats()["resamples"] < 177
