@@ -38,6 +38,11 @@ WORKLOADS = {
                    desc="ClaDS2 lineage-specific-rate birth-death on tree90"),
     "seir": dict(config=3, model="seir", n=1_000_000,
                  desc="vector-borne-disease SEIR on the synthetic 182-day case series seir182"),
+    "geometric": dict(config=None, model="geometric", n=1_000_000,
+                      desc="weighted geometric, Fig. 2 (p=0.5, w=1.5): particles reach b_stop at "
+                           "different epochs (universal control flow, SURVEY f4)"),
+    "ssm": dict(config=None, model="ssm", n=1_000_000,
+                desc="linear-Gaussian state-space model, Eq. (2), 50 synthetic observations (SURVEY f4)"),
     "resample": dict(config=4, model="resample", n=1 << 26,
                      desc="resampling step alone: LSE max + u128 scan + systematic ancestors + 64-B gather"),
 }
@@ -132,6 +137,10 @@ def model_for(smc, wl, rng="lineage"):
         return smc.Model.clads2(inputs.tree(wl["tree"]), inputs.CLADS2_PARAMS, lineage=RNG[rng])
     if wl["model"] == "seir":
         return smc.Model.seir(inputs.seir_series())
+    if wl["model"] == "geometric":
+        return smc.Model.geometric(*inputs.GEOMETRIC_PARAMS)
+    if wl["model"] == "ssm":
+        return smc.Model.ssm(inputs.ssm_series(50), inputs.SSM_PARAMS)
     raise ValueError(wl)
 
 
@@ -143,10 +152,15 @@ def oracle_sweep_rate(wl, budget_s=15.0, n_cap=None):
     import oracle
     lin = getattr(oracle_sweep_rate, "rng", "lineage") == "lineage"
     kind = {"crbd": oracle.CRBD_LR if lin else oracle.CRBD,
-            "clads2": oracle.CLADS2_LR if lin else oracle.CLADS2, "seir": oracle.SEIR}[wl["model"]]
+            "clads2": oracle.CLADS2_LR if lin else oracle.CLADS2, "seir": oracle.SEIR,
+            "geometric": oracle.GEOMETRIC, "ssm": oracle.SSM}[wl["model"]]
     if wl["model"] in ("crbd", "clads2"):
         data = oracle.tree_blob(inputs.tree(wl["tree"]))
         params = inputs.CRBD_PARAMS if wl["model"] == "crbd" else inputs.CLADS2_PARAMS
+    elif wl["model"] == "geometric":
+        data, params = None, inputs.GEOMETRIC_PARAMS
+    elif wl["model"] == "ssm":
+        data, params = inputs.ssm_series(50), inputs.SSM_PARAMS
     else:
         data, params = inputs.seir_series(), None
     n = 1000
@@ -294,13 +308,15 @@ def e2e_sweeps(args, wl, smc, torch, h, model, k_steps, world):
     the handle, re-initialises it with the step's seed, runs the sweep and
     reads back log Z and the final log-weights (D2H).  Host wall clock around
     the whole step, max over ranks."""
-    data = torch.from_numpy(model.data.copy()).pin_memory().numpy()
+    data = (torch.from_numpy(model.data.copy()).pin_memory().numpy() if model.data.size
+            else model.data)
     ts = []
     for k in range(k_steps + 1):
         barrier(torch, world)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        h.set_data(data)
+        if data.size:
+            h.set_data(data)
         h.reset(500 + k)
         h.run()
         lz = h.log_z
@@ -512,6 +528,7 @@ def run_ours(args, wl):
     if not args.no_e2e:
         e = e2e_sweeps(args, wl, smc, torch, r["h"], r["model"], min(args.steps, 3), world)
         tot = sum_over_ranks(torch, world, r["alive_steps"] / args.steps)
+    if not args.no_e2e:
         line["e2e"] = dict(value=tot / e["t"], unit="particle-steps/s",
                            h2d_bytes_per_step=e["h2d"] * world, d2h_bytes_per_step=e["d2h"] * world,
                            note="per step: H2D of the model data, reset(seed), run, D2H of log Z and "
