@@ -434,9 +434,8 @@ int common_init(smc_ctx* h, const smc_model* m, unsigned long long n_per, int wo
     h->lr_grid = (int)std::min<unsigned long long>(batches, (unsigned long long)std::max(1, per_sm) * sms);
     h->tasks.cap = kTasksPerCta;
     const size_t nt = (size_t)h->lr_grid * h->tasks.cap;
-    CU(cudaMalloc(&h->tasks.s, nt * sizeof(double)));
+    CU(cudaMalloc(&h->tasks.sid, nt * sizeof(double2)));
     if (h->kind == SMC_CLADS2) CU(cudaMalloc(&h->tasks.lam, nt * sizeof(double)));
-    CU(cudaMalloc(&h->tasks.id, nt * sizeof(unsigned long long)));
     CU(cudaMalloc(&h->tasks.owner, nt * sizeof(unsigned short)));
   }
   h->shards.resize(n_local_shards);
@@ -845,7 +844,7 @@ void smc_destroy(smc_handle h) {
     cudaFree(s.ctrl); cudaFree(s.d_dst_planes[0]); cudaFree(s.d_dst_planes[1]); cudaFree(s.d_dst_anc);
   }
   cudaFree(h->d_table); cudaFree(h->d_logfact); cudaFree(h->d_recA); cudaFree(h->d_recB); cudaFree(h->d_barrier);
-  cudaFree(h->tasks.s); cudaFree(h->tasks.lam); cudaFree(h->tasks.id); cudaFree(h->tasks.owner);
+  cudaFree(h->tasks.sid); cudaFree(h->tasks.lam); cudaFree(h->tasks.owner);
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
   if (h->graph) cudaGraphDestroy(h->graph);
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);

@@ -42,10 +42,9 @@ constexpr unsigned kTasksPerCta = (unsigned)(kLRThreads * kSeg + kOverflowCap);
 constexpr unsigned kTagNode = 3u, kTagChild = 4u, kTagZ = 5u;
 
 struct TaskArrays {
-  double* s;                    // start age of the lineage
+  double2* sid;                 // (start age of the lineage, 64-bit node id as double bits)
   double* lam;                  // lineage rate (ClaDS2 only; may be null)
-  unsigned long long* id;       // 64-bit node id (id0 | id1 << 32)
-  unsigned short* owner;        // particle slot within the CTA's batch
+  unsigned short* owner;        // particle slot within the batch (overflow region only)
   unsigned cap;                 // tasks per CTA
 };
 
@@ -260,26 +259,35 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
   const double rho = C.p[0];
   const int tid = threadIdx.x;
   const unsigned long long tbase = (unsigned long long)blockIdx.x * kTasksPerCta;
-  double* T_s = a.t.s + tbase;
+  double2* T_sid = a.t.sid + tbase;
   double* T_lam = M::kHasLam ? a.t.lam + tbase : nullptr;
-  unsigned long long* T_id = a.t.id + tbase;
   unsigned short* T_own = a.t.owner + tbase;
   if (tid == 0) s_taskcap = 0;
-  // push a task for owner o: its segment, else the overflow stack
-  auto push_task = [&](int o, double s0, double lam0, unsigned long long id) {
-    int pos = atomicAdd(&s_cnt[o], 1);
-    unsigned long long slot;
-    if (pos < kSeg) {
-      slot = (unsigned long long)o * kSeg + pos;
-    } else {
-      const int q = atomicAdd(&s_ovtop, 1);
-      if (q >= kOverflowCap) { s_taskcap = 1; return; }
-      slot = (unsigned long long)kLRThreads * kSeg + q;
-    }
-    T_s[slot] = s0;
+  // store a task at a CTA-local slot; segment slots imply their owner
+  auto put = [&](unsigned long long slot, int o, double s0, double lam0, unsigned long long id) {
+    T_sid[slot] = make_double2(s0, __longlong_as_double((long long)id));
     if (M::kHasLam) T_lam[slot] = lam0;
-    T_id[slot] = id;
-    T_own[slot] = (unsigned short)o;
+    if (slot >= (unsigned long long)kLRThreads * kSeg) T_own[slot] = (unsigned short)o;
+  };
+  auto overflow_slot = [&]() -> long long {
+    const int q = atomicAdd(&s_ovtop, 1);
+    if (q >= kOverflowCap) { s_taskcap = 1; return -1; }
+    return (long long)kLRThreads * kSeg + q;
+  };
+  // push one task for owner o: its segment, else the overflow stack
+  auto push_task = [&](int o, double s0, double lam0, unsigned long long id) {
+    const int pos = atomicAdd(&s_cnt[o], 1);
+    const long long slot = pos < kSeg ? (long long)o * kSeg + pos : overflow_slot();
+    if (slot >= 0) put((unsigned long long)slot, o, s0, lam0, id);
+  };
+  // push both daughters of a birth with one reservation (first daughter on top)
+  auto push_pair = [&](int o, double s0, double lb, unsigned long long idb, double la,
+                       unsigned long long ida) {
+    const int pos = atomicAdd(&s_cnt[o], 2);
+    const long long s1 = pos < kSeg ? (long long)o * kSeg + pos : overflow_slot();
+    const long long s2 = pos + 1 < kSeg ? (long long)o * kSeg + pos + 1 : overflow_slot();
+    if (s1 >= 0) put((unsigned long long)s1, o, s0, lb, idb);
+    if (s2 >= 0) put((unsigned long long)s2, o, s0, la, ida);
   };
 
   long long key = LLONG_MIN;
@@ -353,6 +361,12 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
         const int off = woff + incl - m;
         const int seg = tid * kSeg;
         for (int j = 0; j < m; ++j) s_sel[off + j] = seg + (c - 1 - j);
+        // side-tree node count of the branch: every popped task of a live owner
+        // is evaluated this round (exact for the node-cap rule, no atomics)
+        if (m && s_dead[tid] == 0) {
+          s_nodes[tid] += (unsigned)m;
+          if (s_nodes[tid] > kSideNodeCap) atomicCAS(&s_dead[tid], 0, 2);
+        }
       }
       __syncthreads();
       // lane -> task
@@ -369,10 +383,11 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
         have = true;
       }
       if (have) {
-        ts = T_s[slot];
+        const double2 rec = T_sid[slot];
+        ts = rec.x;
+        tidv = (unsigned long long)__double_as_longlong(rec.y);
         if (M::kHasLam) tl = T_lam[slot];
-        tidv = T_id[slot];
-        o = T_own[slot];
+        o = slot < (unsigned long long)kLRThreads * kSeg ? (int)(slot / kSeg) : (int)T_own[slot];
       }
       __syncthreads();
       s_cnt[tid] = c - m;
@@ -381,20 +396,14 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
       // s_dead is a sticky flag (0 -> nonzero, never back): written and read
       // with shared-memory atomics; a stale 0 only costs one pruned-late node
       if (have && atomicAdd(&s_dead[o], 0) == 0) {
-        const unsigned cnt = atomicAdd(&s_nodes[o], 1u) + 1u;
-        if (cnt > kSideNodeCap) {
-          atomicCAS(&s_dead[o], 0, 2);
-        } else {
-          const uint32_t n_owner = (uint32_t)(p.shard_base + (unsigned long long)batch * kLRThreads + o);
-          drw += 2;
-          NodeOut out;
-          const int res = M::node(ts, tl, tidv, s_own[o], n_owner, epoch, seed, rho, out);
-          if (res == NODE_DETECTED) {
-            atomicCAS(&s_dead[o], 0, 1);
-          } else if (res == NODE_BIRTH) {
-            push_task(o, out.s2, out.lb, out.idb);
-            push_task(o, out.s2, out.la, out.ida);     // first daughter on top (DFS order)
-          }
+        const uint32_t n_owner = (uint32_t)(p.shard_base + (unsigned long long)batch * kLRThreads + o);
+        drw += 2;
+        NodeOut out;
+        const int res = M::node(ts, tl, tidv, s_own[o], n_owner, epoch, seed, rho, out);
+        if (res == NODE_DETECTED) {
+          atomicCAS(&s_dead[o], 0, 1);
+        } else if (res == NODE_BIRTH) {
+          push_pair(o, out.s2, out.lb, out.idb, out.la, out.ida);   // first daughter on top
         }
       }
       __syncthreads();
