@@ -24,7 +24,7 @@ _lock = threading.Lock()
 _lib = None
 
 # model kinds (same numbering as the public header, redeclared here on purpose)
-CRBD, CLADS2, SEIR, CRBD_LR, CLADS2_LR, GEOMETRIC, SSM, CONSTW = 1, 2, 3, 4, 5, 10, 11, 12
+CRBD, CLADS2, SEIR, CRBD_LR, CLADS2_LR, CRBD_AE, GEOMETRIC, SSM, CONSTW = 1, 2, 3, 4, 5, 6, 10, 11, 12
 OK, EINVAL, EREJECTED, ENAN = 0, 1, 4, 5
 DIST = {"exp": 0, "bernoulli": 1, "uniform": 2, "normal": 3, "gamma": 4, "beta": 5, "binomial": 6}
 
@@ -53,6 +53,8 @@ def lib():
             L.oracle_sample.argtypes = [i32, P(d), u64, u64, P(d), P(u32)]
             L.oracle_binomial_logpmf.argtypes = [i64, i64, d]
             L.oracle_binomial_logpmf.restype = d
+            L.oracle_crbd_E.argtypes = [d, d, d, d]
+            L.oracle_crbd_E.restype = d
             L.oracle_normal_logpdf.argtypes = [d, d, d]
             L.oracle_normal_logpdf.restype = d
             L.oracle_u128_to_double.argtypes = [u64, u64]

@@ -274,9 +274,30 @@ void preorder_smaller(const Tree& T, int v, std::vector<Branch>& out, int& maxpe
 }
 
 // ---- CRBD ----------------------------
+// E(t): probability that a lineage alive at age t leaves no sampled
+// descendant at the present (Nee et al. 1994), the textbook
+//   E(t) = 1 - rho r / (rho lam + (lam (1 - rho) - mu) e^{-r t}),  r = lam - mu,
+// rewritten without cancellation or overflow: with
+// h = (e^{r t} - 1)/r (h = t at r = 0),  E = (rho mu h + 1 - rho)/(rho lam h + 1);
+// for r > 0 numerator and denominator are multiplied by e^{-r t}.
+double crbd_E(double t, double lam, double mu, double rho) {
+  const double r = lam - mu;
+  if (r > 0.0) {
+    const double e = std::exp(-r * t), f = -std::expm1(-r * t) / r;
+    return (rho * mu * f + (1.0 - rho) * e) / (rho * lam * f + e);
+  }
+  const double h = r == 0.0 ? t : std::expm1(r * t) / r;
+  return (rho * mu * h + (1.0 - rho)) / (rho * lam * h + 1.0);
+}
+
 struct CrbdModel {
   std::vector<Branch> br;
   double rho = 1.0, lam_fixed = -1.0, mu_fixed = -1.0;
+  // §5.3 variance reduction: a hidden
+  // speciation event at age t contributes 2 E(t), the probability-weighted
+  // form of "2 if its side tree goes undetected, else 0", instead of a
+  // simulated side tree.
+  bool analytic = false;
   uint64_t stack_cap = 1024, event_cap = (1u << 22);
   struct State { int pc = 0; int branch = 0; double lambda = 0, mu = 0; };
   static const int NF = 4;
@@ -328,6 +349,11 @@ struct CrbdModel {
     for (;;) {
       t = t - sample_exp(rs, s.lambda);
       if (t <= b.tc) break;
+      if (analytic) {
+        lw = lw + LN2;
+        lw = lw + std::log(crbd_E(t, s.lambda, s.mu, rho));
+        continue;
+      }
       int r = undetected(t, s, rs);
       if (r == 1) { lw = lw + LN2; continue; }
       if (r < 0) ++overflow;
@@ -1048,10 +1074,12 @@ thread_local std::string g_err;
 // =============================================================================
 extern "C" {
 
-enum { K_CRBD = 1, K_CLADS2 = 2, K_SEIR = 3, K_CRBD_LR = 4, K_CLADS2_LR = 5,
+enum { K_CRBD = 1, K_CLADS2 = 2, K_SEIR = 3, K_CRBD_LR = 4, K_CLADS2_LR = 5, K_CRBD_AE = 6,
        K_GEOMETRIC = 10, K_SSM = 11, K_CONSTW = 12 };
 
 const char* oracle_errmsg() { return g_err.c_str(); }
+
+double oracle_crbd_E(double t, double lam, double mu, double rho) { return crbd_E(t, lam, mu, rho); }
 
 void oracle_philox(const uint32_t* ctr, const uint32_t* key, uint32_t* out) {
   Block b = philox4x32_10(ctr[0], ctr[1], ctr[2], ctr[3], key[0], key[1]);
@@ -1148,12 +1176,14 @@ void* oracle_smc_create(int kind, const double* data, uint64_t data_len,
   if (N == 0 || N > 0xFFFFFFFFull) { g_err = "N must be in [1, 2^32)"; return nullptr; }
   auto P = [&](int i, double dflt) { return (prm && i < n_prm) ? prm[i] : dflt; };
   switch (kind) {
-    case K_CRBD: {
+    case K_CRBD:
+    case K_CRBD_AE: {
       bool ok; Tree T = parse_tree(data, data_len, ok);
       if (!ok) { g_err = "bad tree"; return nullptr; }
       CrbdModel m;
       preorder_left(T, T.root, m.br);
       m.rho = P(0, 1.0); m.lam_fixed = P(1, -1.0); m.mu_fixed = P(2, -1.0);
+      m.analytic = kind == K_CRBD_AE;
       return new Smc<CrbdModel>(m, N, seed);
     }
     case K_CLADS2: {

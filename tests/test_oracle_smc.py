@@ -117,7 +117,8 @@ def test_ssm_vs_kalman():
     mean_ratio_within_3se(lz, ref)
 
 
-CRBD_KINDS = pytest.mark.parametrize("kind", [oracle.CRBD, oracle.CRBD_LR], ids=["seq", "lineage"])
+CRBD_KINDS = pytest.mark.parametrize("kind", [oracle.CRBD, oracle.CRBD_LR, oracle.CRBD_AE],
+                                     ids=["seq", "lineage", "analytic"])
 
 
 @CRBD_KINDS
@@ -152,6 +153,46 @@ def test_crbd_rho_half_unbiased(kind):
     lz = [run(kind, oracle.tree_blob(TREE5), [0.5, 0.3, 0.1], 1000, s)[0].log_z
           for s in range(1, 101)]
     mean_ratio_within_3se(lz, ref)
+
+
+# ---------------------------------------------------------------- §R-20 analytic E(t)
+@pytest.mark.parametrize("lam,mu,rho", [(0.3, 0.1, 1.0), (0.2, 0.5, 1.0), (0.4, 0.4, 1.0), (0.4, 0.4 + 1e-9, 1.0),
+                                        (0.7, 0.0, 1.0), (1.1, 0.6, 0.5), (0.2, 0.9, 0.3), (3.0, 1.0, 1.0)])
+def test_crbd_E_matches_ode(lam, mu, rho):
+    # E solves dE/dt = mu - (lam+mu) E + lam E^2, E(0) = 1 - rho
+    for t in (1e-9, 0.01, 0.5, 3.0, 10.0):
+        _, e_ode = cf.crbd_branch_ratio_ode(0.0, t, lam, mu, rho)
+        e = oracle.lib().oracle_crbd_E(t, lam, mu, rho)
+        assert e == pytest.approx(e_ode, rel=1e-8, abs=1e-13), (t, e, e_ode)
+    assert oracle.lib().oracle_crbd_E(0.0, lam, mu, rho) == pytest.approx(1.0 - rho, abs=1e-15)
+
+
+def test_crbd_E_extremes():
+    E = oracle.lib().oracle_crbd_E
+    assert E(1e4, 60.0, 1.0, 1.0) == pytest.approx(1.0 / 60.0, rel=1e-12)   # -> mu/lam (supercritical)
+    assert E(1e4, 1.0, 60.0, 1.0) == pytest.approx(1.0, abs=1e-12)          # -> 1 (subcritical)
+    assert E(5.0, 0.7, 0.0, 1.0) == 0.0                                     # Yule, complete sampling
+    assert math.isfinite(E(800.0, 2.0, 1.0, 0.5)) and math.isfinite(E(800.0, 1.0, 2.0, 0.5))
+
+
+def test_crbd_analytic_equals_simulated_when_E_is_zero():
+    # mu = 0, rho = 1: every hidden side tree is detected (simulation) and
+    # E = 0 (analytic); both kinds consume the same draws up to the first
+    # hidden event, so weights, ancestors and log Z agree exactly
+    a, ra = run(oracle.CRBD, oracle.tree_blob(TREE5), [1.0, 0.4, 0.0], 500, 11)
+    b, rb = run(oracle.CRBD_AE, oracle.tree_blob(TREE5), [1.0, 0.4, 0.0], 500, 11)
+    assert ra == rb == oracle.OK
+    assert a.log_z == b.log_z
+    np.testing.assert_array_equal(a.anc(), b.anc())
+    np.testing.assert_array_equal(a.lw(), b.lw())
+
+
+def test_crbd_analytic_reduces_variance():
+    ref = cf.crbd_log_lik(TREE5, 0.3, 0.1)
+    sims = [run(oracle.CRBD, oracle.tree_blob(TREE5), [1.0, 0.3, 0.1], 300, s)[0].log_z for s in range(1, 41)]
+    anas = [run(oracle.CRBD_AE, oracle.tree_blob(TREE5), [1.0, 0.3, 0.1], 300, s)[0].log_z for s in range(1, 41)]
+    assert np.std(anas) < np.std(sims)
+    assert abs(np.mean(anas) - ref) < 0.05
 
 
 def test_crbd_epochs_and_draws():
