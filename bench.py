@@ -34,6 +34,10 @@ import inputs  # noqa: E402
 WORKLOADS = {
     "crbd": dict(config=1, model="crbd", tree="tree90", n=1_000_000,
                  desc="CRBD birth-death, synthetic 90-tip Yule tree (tree90), priors Gamma(1,1)/Gamma(1,0.5)"),
+    "crbd_vr": dict(config=None, model="crbd", tree="tree90", n=1_000_000, analytic=True, ess="1/2",
+                    desc="CRBD on tree90 with the Sec. 5.3 variance reduction: 2E(t) per hidden event "
+                         "instead of a simulated side tree (DESIGN R-20) and ESS-triggered resampling "
+                         "at ESS < N/2 (R-19)"),
     "clads2": dict(config=2, model="clads2", tree="tree90", n=1_000_000,
                    desc="ClaDS2 lineage-specific-rate birth-death on tree90"),
     "seir": dict(config=3, model="seir", n=1_000_000,
@@ -132,7 +136,8 @@ RNG = {"lineage": True, "sequential": False}
 
 def model_for(smc, wl, rng="lineage"):
     if wl["model"] == "crbd":
-        return smc.Model.crbd(inputs.tree(wl["tree"]), inputs.CRBD_PARAMS, lineage=RNG[rng])
+        return smc.Model.crbd(inputs.tree(wl["tree"]), inputs.CRBD_PARAMS, lineage=RNG[rng],
+                              analytic=wl.get("analytic", False))
     if wl["model"] == "clads2":
         return smc.Model.clads2(inputs.tree(wl["tree"]), inputs.CLADS2_PARAMS, lineage=RNG[rng])
     if wl["model"] == "seir":
@@ -151,7 +156,7 @@ def oracle_sweep_rate(wl, budget_s=15.0, n_cap=None):
     roughly budget_s.  Returns (particle-steps/s, sample description, seconds)."""
     import oracle
     lin = getattr(oracle_sweep_rate, "rng", "lineage") == "lineage"
-    kind = {"crbd": oracle.CRBD_LR if lin else oracle.CRBD,
+    kind = {"crbd": (oracle.CRBD_AE if wl.get("analytic") else oracle.CRBD_LR if lin else oracle.CRBD),
             "clads2": oracle.CLADS2_LR if lin else oracle.CLADS2, "seir": oracle.SEIR,
             "geometric": oracle.GEOMETRIC, "ssm": oracle.SSM}[wl["model"]]
     if wl["model"] in ("crbd", "clads2"):
@@ -165,7 +170,9 @@ def oracle_sweep_rate(wl, budget_s=15.0, n_cap=None):
         data, params = inputs.seir_series(), None
     n = 1000
     t0 = time.perf_counter()
+    ea, eb = (int(x) for x in getattr(oracle_sweep_rate, "ess", "1/1").split("/"))
     s = oracle.Smc(kind, data, params, n, 12345)
+    s.set_ess(ea, eb)
     s.run()
     dt = time.perf_counter() - t0
     n = max(1000, int(n * budget_s / max(dt, 1e-3)))
@@ -173,6 +180,7 @@ def oracle_sweep_rate(wl, budget_s=15.0, n_cap=None):
         n = min(n, n_cap)
     t0 = time.perf_counter()
     s = oracle.Smc(kind, data, params, n, 12345)
+    s.set_ess(ea, eb)
     s.run()
     dt = time.perf_counter() - t0
     st = s.stats()
@@ -219,7 +227,7 @@ def run_reference(args, wl):
         line = dict(metric="particle-steps/s", value=v, unit="particle-steps/s", impl="reference")
     line.update(n_gpus=world, steps=args.steps, warmup=args.warmup, higher_is_better=True,
                 scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
-                config=dict(workload=args.workload, desc=wl["desc"], rng=args.rng),
+                config=dict(workload=args.workload, desc=wl["desc"], rng=args.rng, ess_threshold=args.ess),
                 cpu_baseline=dict(value=v, unit=line["unit"], cores=ncores, kind="oracle",
                                   sample=sample),
                 e2e=dict(value=v, unit=line["unit"], h2d_bytes_per_step=0, d2h_bytes_per_step=0))
@@ -502,7 +510,8 @@ def run_ours(args, wl):
                 ms_per_step=r["t_ms"] / args.steps, higher_is_better=True, scaling="weak",
                 vs_baseline=None, dtype="f64", data="synthetic",
                 config=dict(workload=args.workload, desc=wl["desc"], n_per_gpu=N,
-                            rng=args.rng if wl["model"] in ("crbd", "clads2") else "sequential",
+                            rng=("analytic (no side trees)" if wl.get("analytic") else
+                                 args.rng if wl["model"] in ("crbd", "clads2") else "sequential"),
                             ess_threshold=args.ess,
                             epochs_per_sweep=r["epochs"] // args.steps,
                             l2="flushed between steps (state fits L2 within a sweep)"),
@@ -517,12 +526,12 @@ def run_ours(args, wl):
                                        note="reduce + anc_gather + finalize per epoch at this N "
                                             "(latency-bound at 10^6; see workload 'resample')"),
                 roofline=dict(bound="alu",
-                              kernel=("propagate_lr_kernel" if args.rng == "lineage" and wl["model"] != "seir"
-                                      else "propagate_kernel") + f"<{wl['model']}>",
+                              kernel=("propagate_lr_kernel" if args.rng == "lineage" and wl["model"] in ("crbd", "clads2")
+                                      and not wl.get("analytic") else "propagate_kernel") + f"<{args.workload}>",
                               achieved=draw_rate, peak=draw_peak, unit="Gdraws/s",
                               frac=draw_rate / draw_peak,
                               traffic=((traffic(f"{wl['model']}:{N}:propagate_lr_kernel") or {}).get("bytes")
-                                       if args.rng == "lineage" else None),
+                                       if args.rng == "lineage" and not wl.get("analytic") else None),
                               peak_source=f"derived: 148 SM x 128 lanes x {f_max/1e6:.0f} MHz / 34 instr per uniform (DESIGN.md s7)"),
                 gpu_launches=r["launches"], clocks=r["clocks"])
     if not args.no_e2e:
@@ -553,8 +562,9 @@ def main():
     ap.add_argument("--rng", default="lineage", choices=sorted(RNG),
                     help="tree models: lineage-keyed side trees (DESIGN R-18, cooperative kernel) "
                          "or the sequential per-particle stream (R-11)")
-    ap.add_argument("--ess", default="1/1",
-                    help="ESS-adaptive resampling threshold a/b (DESIGN R-19); 1/1 = every checkpoint")
+    ap.add_argument("--ess", default=None,
+                    help="ESS-adaptive resampling threshold a/b (DESIGN R-19); 1/1 = every checkpoint "
+                         "(default: the workload's, 1/1 unless stated)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
@@ -564,7 +574,10 @@ def main():
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 breaks the timing rules", file=sys.stderr)
     wl = WORKLOADS[args.workload]
+    if args.ess is None:
+        args.ess = wl.get("ess", "1/1")
     oracle_sweep_rate.rng = args.rng
+    oracle_sweep_rate.ess = args.ess
     if args.impl == "reference":
         run_reference(args, wl)
     else:

@@ -72,6 +72,13 @@ typedef enum {
  * side trees in parallel (cooperative kernel).  Same model, different (equally
  * valid) stream layout; results match the oracle's lineage-keyed kinds. */
 #define SMC_FLAG_LINEAGE_RNG 2u
+/* CRBD only: the §5.3 variance reduction:
+ * each hidden speciation event at age t contributes ln 2 + ln E(t), E(t) the
+ * probability that a lineage alive at age t leaves no sampled descendant,
+ * instead of a simulated side tree.  Overrides SMC_FLAG_LINEAGE_RNG (no side
+ * trees are simulated).  CLADS2 with this flag: SMC_EINVAL (lineage-specific
+ * rates have no closed-form E). */
+#define SMC_FLAG_ANALYTIC_UNDETECTED 4u
 
 /*
  * Model description (all arrays COPIED at create).

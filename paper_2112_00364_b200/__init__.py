@@ -28,6 +28,7 @@ OK, EINVAL, ECUDA, ENCCL, EREJECTED, ENAN, EOVERFLOW, ESTATE = range(8)
 CRBD, CLADS2, SEIR, GEOMETRIC, SSM, CONSTW, RESAMPLE_BENCH = 1, 2, 3, 10, 11, 12, 20
 FLAG_STRICT = 1
 FLAG_LINEAGE_RNG = 2
+FLAG_ANALYTIC_UNDETECTED = 4
 
 FIELDS = {
     CRBD: ["pc", "branch", "lambda", "mu"],
@@ -166,8 +167,10 @@ class Model:
                            _dptr(self.params), self.params.size, flags)
 
     @staticmethod
-    def crbd(tree, params=(1.0, -1.0, -1.0), flags=0, lineage=False):
-        return Model(CRBD, tree_data(tree), params, flags=flags | (FLAG_LINEAGE_RNG if lineage else 0))
+    def crbd(tree, params=(1.0, -1.0, -1.0), flags=0, lineage=False, analytic=False):
+        """analytic: the §5.3 variance reduction (2 E(t) per hidden event)."""
+        return Model(CRBD, tree_data(tree), params,
+                     flags=flags | (FLAG_LINEAGE_RNG if lineage else 0) | (FLAG_ANALYTIC_UNDETECTED if analytic else 0))
 
     @staticmethod
     def clads2(tree, params=(1.0, -1.0, -1.0, -1.0, -1.0), flags=0, lineage=False):
@@ -217,9 +220,9 @@ class Smc:
             self.set_stream(stream)
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _lib is not None:
             _lib.smc_destroy(self.h)
-            self.h = None
+        self.h = None
 
     __del__ = close
 
@@ -326,9 +329,9 @@ class Resampler:
             _check(self.h, _lib.smc_set_stream(self.h, C.c_void_p(_stream_ptr(stream))))
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _lib is not None:
             _lib.smc_destroy(self.h)
-            self.h = None
+        self.h = None
 
     __del__ = close
 

@@ -83,7 +83,9 @@ enum CommKind { COMM_LOCAL = 0, COMM_NCCL = 1, COMM_CALLBACK = 2 };
 struct smc_ctx {
   int kind = 0;
   bool lineage = false;           // §R-18 lineage-keyed side trees (SMC_FLAG_LINEAGE_RNG)
+  bool analytic = false;          // §R-20 CRBD with 2E(t) per hidden event (SMC_FLAG_ANALYTIC_UNDETECTED)
   int lr_grid = 0;                // persistent grid of the cooperative kernel
+  int prop_grid = 0;              // resident-CTA grid of propagate_kernel<M> (grid-stride)
   TaskArrays tasks{};
   int planes = 0;                 // 16-byte planes per particle
   uint32_t flags = 0;
@@ -231,7 +233,11 @@ int setup_model(smc_ctx* h, const smc_model* m) {
   if (!m) return fail(h, SMC_EINVAL, "model is NULL");
   h->kind = m->kind;
   h->flags = m->flags;
-  h->lineage = (m->flags & SMC_FLAG_LINEAGE_RNG) && (m->kind == SMC_CRBD || m->kind == SMC_CLADS2);
+  h->analytic = (m->flags & SMC_FLAG_ANALYTIC_UNDETECTED) != 0;
+  if (h->analytic && m->kind != SMC_CRBD)
+    return fail(h, SMC_EINVAL, "SMC_FLAG_ANALYTIC_UNDETECTED applies to SMC_CRBD only");
+  h->lineage = !h->analytic && (m->flags & SMC_FLAG_LINEAGE_RNG) &&
+               (m->kind == SMC_CRBD || m->kind == SMC_CLADS2);
   for (int i = 0; i < 12; ++i) h->mc.p[i] = 0.0;
   auto P = [&](int i, double dflt) { return (m->params && i < m->n_params) ? m->params[i] : dflt; };
   std::string err;
@@ -497,8 +503,21 @@ void launch_prop(smc_ctx* h, Shard& s, int cur) {
   a.world = h->world;
   a.rank = s.id;
   a.ctrl = s.ctrl;
-  const unsigned grid = (unsigned)((h->n_per + kThreads - 1) / kThreads);
-  propagate_kernel<M><<<grid, kThreads, 0, h->stream>>>(a, h->mc);
+  if (!h->prop_grid) {
+    // light models: one wave of resident CTAs (the kernel grid-strides), so the
+    // epilogue's same-address atomics run once per CTA; uneven models: one CTA
+    // per 256 particles.  Occupancy query only, nothing enqueued (safe during
+    // graph capture)
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, propagate_kernel<M>, kThreads, 0);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned long long need = (h->n_per + kThreads - 1) / kThreads;
+    h->prop_grid = M::kOneWave
+        ? (int)std::min<unsigned long long>(need, (unsigned long long)std::max(1, per_sm * sms))
+        : (int)need;
+  }
+  propagate_kernel<M><<<(unsigned)h->prop_grid, kThreads, 0, h->stream>>>(a, h->mc);
 }
 template <class M>
 void launch_prop_lr(smc_ctx* h, Shard& s, int cur) {
@@ -522,7 +541,10 @@ void launch_propagate(smc_ctx* h, Shard& s, int cur) {
     return;
   }
   switch (h->kind) {
-    case SMC_CRBD: launch_prop<Crbd>(h, s, cur); break;
+    case SMC_CRBD:
+      if (h->analytic) launch_prop<CrbdAE>(h, s, cur);
+      else launch_prop<Crbd>(h, s, cur);
+      break;
     case SMC_CLADS2: launch_prop<Clads2>(h, s, cur); break;
     case SMC_SEIR: launch_prop<Seir>(h, s, cur); break;
     case SMC_GEOMETRIC: launch_prop<Geometric>(h, s, cur); break;

@@ -257,8 +257,48 @@ struct PropArgs {
   Ctrl* ctrl;
 };
 
+// Per-thread accumulators of propagate_kernel's epilogue.
+struct PropAcc {
+  int start_alive = 0, end_alive = 0;
+  bool bad = false;
+  unsigned long long drw = 0, first_bad = ~0ull;
+  long long key = LLONG_MIN;
+};
+
+// One particle: load, run blocks to the next checkpoint (or STOP), store.
+template <class M>
+__device__ __forceinline__ void propagate_one(const PropArgs& a, const ModelConst& C, unsigned long long i,
+                                              unsigned epoch, bool carry, unsigned long long seed,
+                                              PropAcc& acc, Diag& dg) {
+  double lw = carry ? a.lw[i] : 0.0;
+  const unsigned long long ovf0 = dg.overflow;
+  typename M::State s;
+  M::load(s, a.planes, a.n_local, i);
+  if (M::pc(s) != kStop) {
+    ++acc.start_alive;
+    Rng r(seed, (uint32_t)(a.shard_base + i), epoch);
+    for (;;) {
+      const bool ck = M::step(s, lw, r, C, dg);
+      if (ck || M::pc(s) == kStop) break;
+    }
+    M::store(s, a.planes, a.n_local, i);
+    acc.drw += 2ull * r.blk - (r.has_spare ? 1ull : 0ull);
+  }
+  acc.end_alive += M::pc(s) != kStop;
+  a.lw[i] = lw;
+  const bool b = isnan(lw) || lw == INFINITY;
+  acc.bad |= b;
+  if ((b || dg.overflow != ovf0) && acc.first_bad == ~0ull) acc.first_bad = a.shard_base + i;
+  const long long k = order_key(lw);
+  acc.key = k > acc.key ? k : acc.key;
+}
+
 // Register cap per model (M::kMinBlocks resident CTAs per SM), measured on
 // B200: CRBD 4 (64 regs), SEIR 3 (80 regs; samplers out of line), ClaDS2 2.
+// Grid (M::kOneWave): light models run one wave of resident CTAs and
+// grid-stride, so the epilogue's same-address atomics run once per CTA;
+// uneven models run one particle per thread and let the block scheduler
+// balance the load.
 template <class M>
 __global__ void __launch_bounds__(kThreads, M::kMinBlocks) propagate_kernel(PropArgs a, ModelConst C) {
   __shared__ long long s_key[kThreads / 32];
@@ -266,33 +306,23 @@ __global__ void __launch_bounds__(kThreads, M::kMinBlocks) propagate_kernel(Prop
   __shared__ unsigned long long s_drw[kThreads / 32];
   if (*(volatile unsigned*)&a.ctrl->done) return;
   const unsigned epoch = a.ctrl->epoch;
-  const unsigned long long i = (unsigned long long)blockIdx.x * kThreads + threadIdx.x;
-  const bool valid = i < a.n_local;
   const bool carry = a.ctrl->carry != 0;               // R-19: no resample at the last checkpoint
-  double lw = (valid && carry) ? a.lw[i] : 0.0;
-  int start_alive = 0, end_alive = 0;
-  bool bad = false;
-  unsigned long long drw = 0;
+  const unsigned long long seed = a.ctrl->seed;
+  PropAcc acc;
   Diag dg;
-  if (valid) {
-    typename M::State s;
-    M::load(s, a.planes, a.n_local, i);
-    if (M::pc(s) != kStop) {
-      start_alive = 1;
-      Rng r(a.ctrl->seed, (uint32_t)(a.shard_base + i), epoch);
-      for (;;) {
-        const bool ck = M::step(s, lw, r, C, dg);
-        if (ck || M::pc(s) == kStop) break;
-      }
-      M::store(s, a.planes, a.n_local, i);
-      drw = 2ull * r.blk - (r.has_spare ? 1ull : 0ull);
-    }
-    end_alive = M::pc(s) != kStop;
-    a.lw[i] = lw;
-    bad = isnan(lw) || lw == INFINITY;
+  const unsigned long long i0 = (unsigned long long)blockIdx.x * kThreads + threadIdx.x;
+  if constexpr (M::kOneWave) {
+    for (unsigned long long i = i0; i < a.n_local; i += (unsigned long long)gridDim.x * kThreads)
+      propagate_one<M>(a, C, i, epoch, carry, seed, acc, dg);
+  } else {
+    if (i0 < a.n_local) propagate_one<M>(a, C, i0, epoch, carry, seed, acc, dg);
   }
+  int start_alive = acc.start_alive, end_alive = acc.end_alive;
+  const bool bad = acc.bad;
+  unsigned long long drw = acc.drw;
+  const unsigned long long first_bad = acc.first_bad;
+  long long key = acc.key;
   // epilogue: CTA max key, counts, flags
-  long long key = valid ? order_key(lw) : LLONG_MIN;
   unsigned long long ovf = dg.overflow;
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {
@@ -303,20 +333,26 @@ __global__ void __launch_bounds__(kThreads, M::kMinBlocks) propagate_kernel(Prop
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) { s_key[warp] = key; s_ovf[warp] = ovf; s_drw[warp] = drw; }
-  if (dg.overflow || bad) atomicMin(&a.ctrl->first_err, a.shard_base + i);
-  __syncwarp();   // bar.red needs a converged warp (synccheck)
-  const int n_end = __syncthreads_count(end_alive);
-  __syncwarp();   // bar.red needs a converged warp (synccheck)
-  const int n_start = __syncthreads_count(start_alive);
+  if (first_bad != ~0ull) atomicMin(&a.ctrl->first_err, first_bad);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    end_alive += __shfl_xor_sync(0xffffffffu, end_alive, d);
+    start_alive += __shfl_xor_sync(0xffffffffu, start_alive, d);
+  }
+  __shared__ int s_cnt2[2][kThreads / 32];
+  if (lane == 0) { s_cnt2[0][warp] = end_alive; s_cnt2[1][warp] = start_alive; }
   __syncwarp();   // bar.red needs a converged warp (synccheck)
   const int any_bad = __syncthreads_or(bad);
   if (threadIdx.x == 0) {
     long long k = s_key[0];
     unsigned long long o = s_ovf[0], dr = s_drw[0];
+    int n_end = s_cnt2[0][0], n_start = s_cnt2[1][0];
     for (int w = 1; w < kThreads / 32; ++w) {
       k = s_key[w] > k ? s_key[w] : k;
       o += s_ovf[w];
       dr += s_drw[w];
+      n_end += s_cnt2[0][w];
+      n_start += s_cnt2[1][w];
     }
     RecA* rec = a.recA + (epoch & 1) * a.world + a.rank;
     atomicMax(&rec->key, k);
@@ -484,16 +520,25 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(ResArgs a) {
     a.recB[par * a.world + a.rank].W = run;     // shard total
     a.ctrl->counter = 0;
   }
-  if (ess && threadIdx.x == 0) {
+  if (ess) {                                   // uniform: whole CTA
+    // shard sum of q^2: each thread its tile range, then warps, then the CTA
     U192 q = {{0, 0, 0}};
-    for (int t = 0; t < nt; ++t) {
+    for (int t = lo; t < hi; ++t) {
       U192 v;
       const unsigned long long* src = (const unsigned long long*)(a.tile_q2 + t);
       v.w[0] = __ldcg(src); v.w[1] = __ldcg(src + 1); v.w[2] = __ldcg(src + 2);
       add_u192(q, v);
     }
-    RecB* rb = a.recB + par * a.world + a.rank;
-    rb->q2[0] = q.w[0]; rb->q2[1] = q.w[1]; rb->q2[2] = q.w[2];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) add_u192(q, shfl_xor_u192(q, d));
+    if (lane == 0) s_q2[0][warp] = q;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      U192 t = s_q2[0][0];
+      for (int w = 1; w < kThreads / 32; ++w) add_u192(t, s_q2[0][w]);
+      RecB* rb = a.recB + par * a.world + a.rank;
+      rb->q2[0] = t.w[0]; rb->q2[1] = t.w[1]; rb->q2[2] = t.w[2];
+    }
   }
 }
 

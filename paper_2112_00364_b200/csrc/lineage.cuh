@@ -7,22 +7,24 @@
 // nodes, and with one thread per particle that single thread bounds the whole
 // epoch.  Under §R-18 every tree node draws from its own Philox block (counter
 // = node id, particle, epoch, tag), so a tree's nodes can be evaluated in any
-// order.  This kernel therefore runs, per CTA, a batch of 256 particles:
+// order.  This kernel therefore runs, per CTA, a batch of kLRThreads (128)
+// particles:
 //   phase 1  each thread walks its particle's observed branch on the
 //            particle's own stream (INIT, hidden event times, node bookkeeping)
 //            and pushes one root task per hidden event onto the CTA's stack;
 //   phase 2  rounds: every particle ("owner") with pending tasks gets W =
-//            256 / (#owners with tasks) lanes (its top W tasks, LIFO per
-//            owner); lanes left over take tasks from a CTA overflow stack.
+//            128 / (#owners with tasks last round) lanes (its top W tasks,
+//            LIFO per owner, trimmed to the lanes left at its prefix offset);
+//            lanes left over take tasks from a CTA overflow stack.
 //            With many busy owners each explores depth-first (the order a
 //            sequential DFS uses, so a supercritical tree is detected along
-//            one path instead of 256); when few remain, their trees get the
+//            one path instead of 128); when few remain, their trees get the
 //            idle lanes.  Tasks of particles already detected are pruned;
 //   phase 3  each thread finishes its particle: -inf if any node was detected
 //            (or the node cap was exceeded), else + ln 2 per hidden event.
 // The grid is persistent (CTAs pull 256-particle batches from a counter), so a
 // CTA stuck on a giant tree does not hold back the other batches, and the giant
-// tree itself is explored 256 nodes at a time.
+// tree itself is explored 128 nodes at a time.
 #pragma once
 #include "kernels.cuh"
 
@@ -326,21 +328,20 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
         drw += 2ull * r.blk - (r.has_spare ? 1ull : 0ull);
       }
     }
-    __syncthreads();
+    __syncwarp();   // bar.red needs a converged warp (synccheck)
+    int n_act = __syncthreads_count(s_cnt[tid] > 0);
     if (s_cnt[tid] > kSeg) s_cnt[tid] = kSeg;     // pushes beyond the segment went to overflow
-    if (tid == 0 && s_ovtop > kOverflowCap) s_ovtop = kOverflowCap;
     // ---------------- phase 2: cooperative side-tree evaluation
+    // Four barriers per round: (A) scan + active count, (B) lane map written,
+    // (C) task records read, (D) pushes done.  The fair share W uses the
+    // previous round's active-owner count; each owner trims its share to the
+    // lanes left at its prefix offset, so at most kLRThreads tasks are taken.
     unsigned rounds = 0;
     const int warp_id = tid >> 5, lane_id = tid & 31;
     for (;;) {
       const int c = s_cnt[tid];
-      __syncwarp();   // bar.red needs a converged warp (synccheck)
-      const int active = __syncthreads_count(c > 0);
-      const int ov = s_ovtop;
-      if (active == 0 && ov == 0) break;
-      const int W = active ? max(1, kLRThreads / active) : 0;
+      const int W = max(1, kLRThreads / max(1, n_act));
       const int m = min(c, W);
-      // exclusive block scan of m
       int incl = m;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
@@ -348,7 +349,10 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
         if (lane_id >= d) incl += o;
       }
       if (lane_id == 31) s_wsum[warp_id] = incl;
-      __syncthreads();
+      const int ov = min(*(volatile int*)&s_ovtop, kOverflowCap);
+      __syncwarp();   // bar.red needs a converged warp (synccheck)
+      n_act = __syncthreads_count(c > 0);                                  // (A)
+      if (n_act == 0 && ov == 0) break;
       int woff = 0, T = 0;
 #pragma unroll
       for (int w = 0; w < kLRThreads / 32; ++w) {
@@ -356,19 +360,23 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
         woff += w < warp_id ? v : 0;
         T += v;
       }
+      T = min(T, kLRThreads);
       {
         // owner tid writes the slots of its top m tasks to lanes [off, off+m)
         const int off = woff + incl - m;
+        const int me = max(0, min(m, kLRThreads - off));
         const int seg = tid * kSeg;
-        for (int j = 0; j < m; ++j) s_sel[off + j] = seg + (c - 1 - j);
+        for (int j = 0; j < me; ++j) s_sel[off + j] = seg + (c - 1 - j);
+        s_cnt[tid] = c - me;
         // side-tree node count of the branch: every popped task of a live owner
         // is evaluated this round (exact for the node-cap rule, no atomics)
-        if (m && s_dead[tid] == 0) {
-          s_nodes[tid] += (unsigned)m;
+        if (me && s_dead[tid] == 0) {
+          s_nodes[tid] += (unsigned)me;
           if (s_nodes[tid] > kSideNodeCap) atomicCAS(&s_dead[tid], 0, 2);
         }
+        if (tid == 0) s_ovtop = ov - min(ov, kLRThreads - T);
       }
-      __syncthreads();
+      __syncthreads();                                                     // (B)
       // lane -> task
       bool have = false;
       double ts = 0.0, tl = 0.0;
@@ -389,10 +397,7 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
         if (M::kHasLam) tl = T_lam[slot];
         o = slot < (unsigned long long)kLRThreads * kSeg ? (int)(slot / kSeg) : (int)T_own[slot];
       }
-      __syncthreads();
-      s_cnt[tid] = c - m;
-      if (tid == 0) s_ovtop = ov - min(ov, kLRThreads - T);
-      __syncthreads();
+      __syncthreads();                                                     // (C)
       // s_dead is a sticky flag (0 -> nonzero, never back): written and read
       // with shared-memory atomics; a stale 0 only costs one pruned-late node
       if (have && atomicAdd(&s_dead[o], 0) == 0) {
@@ -406,9 +411,8 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
           push_pair(o, out.s2, out.lb, out.idb, out.la, out.ida);   // first daughter on top
         }
       }
-      __syncthreads();
+      __syncthreads();                                                     // (D)
       if (s_cnt[tid] > kSeg) s_cnt[tid] = kSeg;
-      if (tid == 0 && s_ovtop > kOverflowCap) s_ovtop = kOverflowCap;
       ++rounds;
     }
     max_rounds = rounds > max_rounds ? rounds : max_rounds;

@@ -60,6 +60,7 @@ __device__ __forceinline__ double hi_d(uint4 v) {
 struct Crbd {
   static constexpr int kPlanes = 2;
   static constexpr int kMinBlocks = 4;
+  static constexpr bool kOneWave = false;  // grid: one CTA per 256 particles (uneven work: block scheduler balances)
   struct State { double lambda, mu; int pc, branch; };
   __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
     const uint4 a = ldp(P, st, 0, i), b = ldp(P, st, 1, i);
@@ -132,6 +133,55 @@ struct Crbd {
 };
 
 // ============================================================================
+// CRBD with the §5.3 variance reduction: each hidden
+// speciation event at age t is weighted by 2 E(t), E = probability that a
+// lineage alive at age t leaves no sampled descendant, instead of simulating
+// its side tree.  Same state and planes as Crbd; no helper stack.
+// ============================================================================
+__device__ __forceinline__ double crbd_no_sampled_descendant(double t, double lam, double mu, double rho) {
+  // one branch-free form for both signs of r = lam - mu (lanes of a warp hold
+  // different particles' rates): with a = |r| t, g = (1 - e^{-a}) / |r|
+  // (-> t at r = 0) and c = e^{-rt} if r > 0 else 1,
+  //   E = (rho mu g + (1 - rho) c) / (rho lam g + c)
+  // (r > 0: numerator and denominator of the textbook form scaled by e^{-rt})
+  const double r = lam - mu, ar = fabs(r);
+  const double em = expm1(-ar * t);                    // e^{-a} - 1, in (-1, 0]
+  const double g = ar > 0.0 ? -em / ar : t;
+  const double c = r > 0.0 ? exp(-ar * t) : 1.0;       // not em + 1: relative accuracy for large a
+  return (rho * mu * g + (1.0 - rho) * c) / (rho * lam * g + c);
+}
+
+struct CrbdAE : Crbd {
+  static constexpr int kMinBlocks = 4;
+  static constexpr bool kOneWave = true;   // grid: one resident wave, grid-stride (light, even work)
+  __device__ static bool step(State& s, double& lw, Rng& r, const ModelConst& C, Diag&) {
+    const double rho = C.p[0];
+    if (s.pc == 0) {                                    // INIT, jump (no checkpoint)
+      s.lambda = C.p[1] >= 0.0 ? C.p[1] : d_gamma(r, 1.0, 1.0);
+      s.mu = C.p[2] >= 0.0 ? C.p[2] : d_gamma(r, 1.0, 0.5);
+      s.branch = 0;
+      s.pc = 1;
+      return false;
+    }
+    const double* b = C.table + 3 * s.branch;           // BRANCH
+    const double tp = __ldg(b), tc = __ldg(b + 1);
+    const bool internal = __ldg(b + 2) != 0.0;
+    lw = lw + (-s.mu * (tp - tc));
+    lw = lw + (internal ? log(s.lambda) : log(rho));
+    double t = tp;
+    for (;;) {
+      t = t - d_exp(r, s.lambda);
+      if (t <= tc) break;
+      lw = lw + kLn2;
+      lw = lw + log(crbd_no_sampled_descendant(t, s.lambda, s.mu, rho));
+    }
+    s.branch = s.branch + 1;
+    s.pc = (s.branch == C.n) ? kStop : 1;
+    return true;
+  }
+};
+
+// ============================================================================
 // ClaDS2 (§R-14).  Table: per branch i (smaller-subtree-first preorder):
 // [t_parent, t_child, internal, first_left]; C.p[5] = root first_left.
 // Params: rho, lambda0, sigma, alpha, eps (each < 0: prior).
@@ -144,6 +194,7 @@ struct Crbd {
 struct Clads2 {
   static constexpr int kPlanes = 6;
   static constexpr int kMinBlocks = 2;
+  static constexpr bool kOneWave = false;  // grid: one CTA per 256 particles (uneven work: block scheduler balances)
   static constexpr int kPend = 6;
   static constexpr double kMaxRate = 1e4;
   __device__ static bool bad_rate(double r) { return !(r <= kMaxRate); }
@@ -292,6 +343,7 @@ struct Clads2 {
 struct Seir {
   static constexpr int kPlanes = 6;
   static constexpr int kMinBlocks = 3;
+  static constexpr bool kOneWave = false;  // grid: one CTA per 256 particles (uneven work: block scheduler balances)
   struct State { double lam_h, del_h, gam_h, lam_m, del_m, rho; int sh, eh, ih, rh, sm, em, im, t, pc; };
   __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
     uint4 v = ldp(P, st, 0, i); s.lam_h = lo_d(v); s.del_h = hi_d(v);
@@ -369,6 +421,7 @@ struct Seir {
 struct Geometric {
   static constexpr int kPlanes = 1;
   static constexpr int kMinBlocks = 4;
+  static constexpr bool kOneWave = true;   // grid: one resident wave, grid-stride (light, even work)
   struct State { int pc, n; };
   __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
     const uint4 v = ldp(P, st, 0, i); s.pc = (int)v.x; s.n = (int)v.y;
@@ -393,6 +446,7 @@ struct Geometric {
 struct Ssm {
   static constexpr int kPlanes = 1;
   static constexpr int kMinBlocks = 4;
+  static constexpr bool kOneWave = true;   // grid: one resident wave, grid-stride (light, even work)
   struct State { double x; int pc, t; };
   __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
     const uint4 v = ldp(P, st, 0, i); s.x = lo_d(v); s.pc = (int)v.z; s.t = (int)v.w;
@@ -423,6 +477,7 @@ struct Ssm {
 struct Constw {
   static constexpr int kPlanes = 1;
   static constexpr int kMinBlocks = 4;
+  static constexpr bool kOneWave = true;   // grid: one resident wave, grid-stride (light, even work)
   struct State { int pc, k; };
   __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
     const uint4 v = ldp(P, st, 0, i); s.pc = (int)v.x; s.k = (int)v.y;

@@ -22,16 +22,19 @@ pytestmark = pytest.mark.gpu
 RTOL = 1e-9
 
 
-TREE_KINDS = (oracle.CRBD, oracle.CLADS2, oracle.CRBD_LR, oracle.CLADS2_LR)
-LINEAGE = {oracle.CRBD_LR: oracle.CRBD, oracle.CLADS2_LR: oracle.CLADS2}
+TREE_KINDS = (oracle.CRBD, oracle.CLADS2, oracle.CRBD_LR, oracle.CLADS2_LR, oracle.CRBD_AE)
+# oracle kind -> (GPU kind, GPU flag name)
+GPU_KIND = {oracle.CRBD_LR: (oracle.CRBD, "FLAG_LINEAGE_RNG"), oracle.CLADS2_LR: (oracle.CLADS2, "FLAG_LINEAGE_RNG"),
+            oracle.CRBD_AE: (oracle.CRBD, "FLAG_ANALYTIC_UNDETECTED")}
 
 
 def both(smc, kind, tree_or_data, params, N, seed, shards=1):
     """(gpu Smc, oracle Smc) for the same model/N/seed, not yet run.  The
-    oracle's lineage-keyed kinds map to the GPU kind + SMC_FLAG_LINEAGE_RNG."""
+    oracle's lineage-keyed kinds map to the GPU kind + SMC_FLAG_LINEAGE_RNG,
+    the analytic CRBD kind to SMC_CRBD + SMC_FLAG_ANALYTIC_UNDETECTED."""
     if kind in TREE_KINDS:
-        flags = smc.FLAG_LINEAGE_RNG if kind in LINEAGE else 0
-        gm = smc.Model(LINEAGE.get(kind, kind), smc.tree_data(tree_or_data), params, flags=flags)
+        gk, fl = GPU_KIND.get(kind, (kind, None))
+        gm = smc.Model(gk, smc.tree_data(tree_or_data), params, flags=getattr(smc, fl) if fl else 0)
         od = oracle.tree_blob(tree_or_data)
     else:
         gm = smc.Model(kind, tree_or_data, params)
@@ -149,7 +152,8 @@ def test_ssm(smc):
     run_pair(smc, oracle.SSM, inputs.ssm_series(50), inputs.SSM_PARAMS, 3000, 5)
 
 
-CRBD_K = pytest.mark.parametrize("ck", [oracle.CRBD, oracle.CRBD_LR], ids=["seq", "lineage"])
+CRBD_K = pytest.mark.parametrize("ck", [oracle.CRBD, oracle.CRBD_LR, oracle.CRBD_AE],
+                                 ids=["seq", "lineage", "analytic"])
 CLADS_K = pytest.mark.parametrize("ck", [oracle.CLADS2, oracle.CLADS2_LR], ids=["seq", "lineage"])
 
 
@@ -192,6 +196,13 @@ def test_seir(smc):
 def test_seir_tiny_population(smc):
     params = [0.5, 0.4, 0.3, 0.6, 0.5, 0.7, 3, 1, 1, 1]
     run_pair(smc, oracle.SEIR, np.array([1.0, 0.0, 1.0]), params, 3000, 9)
+
+
+def test_analytic_flag_crbd_only(smc):
+    with pytest.raises(smc.SmcError) as e:
+        smc.Smc(smc.Model(smc.CLADS2, smc.tree_data(inputs.tree("tree5")), inputs.CLADS2_PARAMS,
+                          flags=smc.FLAG_ANALYTIC_UNDETECTED), 100, 1)
+    assert e.value.code == smc.EINVAL
 
 
 def test_rejected(smc):
@@ -237,6 +248,7 @@ def test_crbd_full_size_prefix(smc, ck):
 @pytest.mark.parametrize("kind,data,params,N", [
     (oracle.CRBD, "tree90", inputs.CRBD_PARAMS, 5000),
     (oracle.CRBD_LR, "tree90", inputs.CRBD_PARAMS, 5000),
+    (oracle.CRBD_AE, "tree90", inputs.CRBD_PARAMS, 5000),
     (oracle.CLADS2_LR, "tree90", inputs.CLADS2_PARAMS, 3000),
     (oracle.GEOMETRIC, None, inputs.GEOMETRIC_PARAMS, 3001),     # particles stop at different epochs
     (oracle.SEIR, "seir", None, 1500),
@@ -385,7 +397,7 @@ def run_pair_ess(smc, kind, data, params, N, seed, a, b, per_epoch=True, shards=
 
 
 @pytest.mark.parametrize("a,b", [(1, 2), (0, 1), (9, 10)])
-@pytest.mark.parametrize("ck", [oracle.CRBD, oracle.CRBD_LR], ids=["seq", "lineage"])
+@pytest.mark.parametrize("ck", [oracle.CRBD, oracle.CRBD_LR, oracle.CRBD_AE], ids=["seq", "lineage", "analytic"])
 def test_ess_crbd(smc, ck, a, b):
     run_pair_ess(smc, ck, inputs.tree("tree5"), [1.0, 0.3, 0.1], 3000, 5, a, b)
 

@@ -31,10 +31,13 @@ if args.workload == "resample":
 else:
     lin = args.rng == "lineage"
     m = {"crbd": lambda: smc.Model.crbd(inputs.tree("tree90"), lineage=lin),
+         "crbd_vr": lambda: smc.Model.crbd(inputs.tree("tree90"), analytic=True),
          "clads2": lambda: smc.Model.clads2(inputs.tree("tree90"), lineage=lin),
          "seir": lambda: smc.Model.seir(inputs.seir_series())}[args.workload]()
     h = smc.Smc(m, args.n, 1)
     h.set_graph(False)     # ncu does not profile kernels inside conditional-graph bodies
+    if args.workload == "crbd_vr":
+        h.set_ess_threshold(1, 2)
     for s in range(args.sweeps):
         h.reset(1 + s)
         h.run()
