@@ -63,6 +63,8 @@ def lib():
             L.oracle_systematic.argtypes = [P(u64), u64, u64, P(u32)]
             L.oracle_quantize.argtypes = [P(d), u64, P(u64)]
             L.oracle_gather.argtypes = [vp, vp, P(u32), u64, u64]
+            L.oracle_permute.argtypes = [P(u32), u64, P(u32)]
+            L.oracle_smc_set_inplace.argtypes = [vp, i32]
             L.oracle_smc_create.argtypes = [i32, P(d), u64, P(d), i32, u64, u64]
             L.oracle_smc_create.restype = vp
             L.oracle_smc_step.argtypes = [vp, P(i32)]
@@ -198,6 +200,14 @@ def gather(states, anc):
     return out
 
 
+def permute(anc_sorted):
+    """In-place ancestor permutation (R-21) of sorted ancestors."""
+    a = np.ascontiguousarray(anc_sorted, dtype=np.uint32)
+    c = np.zeros_like(a)
+    lib().oracle_permute(_p(a, C.c_uint32), a.size, _p(c, C.c_uint32))
+    return c
+
+
 def tree_blob(tree) -> np.ndarray:
     """Oracle-side encoding of a tree dict (parent/left/right/age/root)."""
     M = len(tree["age"])
@@ -233,6 +243,10 @@ class Smc:
 
     def run(self):
         return lib().oracle_smc_run(self.h)
+
+    def set_inplace(self, on=True):
+        """Permuted ancestors for in-place resampling (R-21)."""
+        lib().oracle_smc_set_inplace(self.h, 1 if on else 0)
 
     def set_ess(self, a, b):
         """ESS threshold tau = a / b (a >= b: resample at every checkpoint)."""

@@ -890,6 +890,23 @@ void systematic(const std::vector<uint64_t>& q, uint64_t N, u128 W, uint64_t z, 
   }
 }
 
+// Ancestor permutation for in-place resampling (SURVEY §8f
+// row f3; the in-place propagation of Murray et al. 2016 that RootPPL does not
+// use).  From the sorted ancestors a: every particle k with offspring
+// keeps its own slot (c_k = k); the remaining copies -- o_k - 1 of each k, in
+// ascending k -- fill the slots of the particles without offspring, in
+// ascending slot order.  c is a permutation of a; no slot without offspring
+// is a source, so the gather can run in place.
+void permute_ancestors(const uint32_t* a, uint64_t N, uint32_t* c) {
+  std::vector<uint64_t> o(N, 0);
+  for (uint64_t j = 0; j < N; ++j) o[a[j]] += 1;
+  std::vector<uint32_t> extras;
+  for (uint64_t k = 0; k < N; ++k)
+    for (uint64_t e = 1; e < o[k]; ++e) extras.push_back((uint32_t)k);
+  uint64_t h = 0;
+  for (uint64_t k = 0; k < N; ++k) c[k] = o[k] > 0 ? (uint32_t)k : extras[h++];
+}
+
 // ESS-adaptive resampling: with
 // integer weights q, ESS = W^2 / sum q^2.  Resample iff tau >= 1 or
 // ESS < tau N, tau = a/b, evaluated exactly:  b W^2 < a N sum q^2.
@@ -955,6 +972,7 @@ struct SmcBase {
   uint32_t ess_a = 1, ess_b = 1;        // tau = a / b (>= 1: resample at every checkpoint)
   double last_ess = 0.0;
   bool carry = false;                   // last checkpoint did not resample: lw accumulates
+  bool inplace = false;                 // R-21: permuted ancestors (in-place gather)
   std::vector<double> lw;
   std::vector<uint32_t> anc;
   std::vector<uint64_t> last_q;
@@ -1036,6 +1054,10 @@ struct Smc : SmcBase {
     // Resampling (Alg. 1 step 3; systematic)
     last.z = resample_z(seed, t);
     systematic(last_q, N, last.W, last.z, anc.data());
+    if (inplace) {
+      std::vector<uint32_t> sorted(anc);
+      permute_ancestors(sorted.data(), N, anc.data());
+    }
     tmp.resize(N);
     for (uint64_t j = 0; j < N; ++j) tmp[j] = st[anc[j]];
     st.swap(tmp);
@@ -1165,6 +1187,8 @@ int oracle_quantize(const double* lw, uint64_t N, uint64_t* q_out) {
 }
 
 // Gather of opaque fixed-size states: out[j] = in[anc[j]] (state_bytes each).
+void oracle_permute(const uint32_t* a, uint64_t N, uint32_t* c) { permute_ancestors(a, N, c); }
+
 void oracle_gather(const uint8_t* in, uint8_t* out, const uint32_t* anc, uint64_t N,
                    uint64_t state_bytes) {
   for (uint64_t j = 0; j < N; ++j)
@@ -1262,6 +1286,11 @@ void* oracle_smc_create(int kind, const double* data, uint64_t data_len,
 
 int oracle_smc_step(void* h, int* done) { return ((SmcBase*)h)->step(done); }
 // ESS threshold tau = a / b (R-19); a >= b: resample at every checkpoint.
+int oracle_smc_set_inplace(void* h, int on) {
+  static_cast<SmcBase*>(h)->inplace = on != 0;
+  return E_OK;
+}
+
 int oracle_smc_set_ess(void* h, uint32_t a, uint32_t b) {
   if (b == 0) return E_INVAL;
   ((SmcBase*)h)->ess_a = a; ((SmcBase*)h)->ess_b = b;
