@@ -134,18 +134,19 @@ def dist_init(gpus):
 RNG = {"lineage": True, "sequential": False}
 
 
-def model_for(smc, wl, rng="lineage"):
+def model_for(smc, wl, rng="lineage", inplace=False):
+    fl = smc.FLAG_INPLACE if inplace else 0
     if wl["model"] == "crbd":
         return smc.Model.crbd(inputs.tree(wl["tree"]), inputs.CRBD_PARAMS, lineage=RNG[rng],
-                              analytic=wl.get("analytic", False))
+                              analytic=wl.get("analytic", False), flags=fl)
     if wl["model"] == "clads2":
-        return smc.Model.clads2(inputs.tree(wl["tree"]), inputs.CLADS2_PARAMS, lineage=RNG[rng])
+        return smc.Model.clads2(inputs.tree(wl["tree"]), inputs.CLADS2_PARAMS, lineage=RNG[rng], flags=fl)
     if wl["model"] == "seir":
-        return smc.Model.seir(inputs.seir_series())
+        return smc.Model.seir(inputs.seir_series(), flags=fl)
     if wl["model"] == "geometric":
-        return smc.Model.geometric(*inputs.GEOMETRIC_PARAMS)
+        return smc.Model.geometric(*inputs.GEOMETRIC_PARAMS, flags=fl)
     if wl["model"] == "ssm":
-        return smc.Model.ssm(inputs.ssm_series(50), inputs.SSM_PARAMS)
+        return smc.Model.ssm(inputs.ssm_series(50), inputs.SSM_PARAMS, flags=fl)
     raise ValueError(wl)
 
 
@@ -173,6 +174,7 @@ def oracle_sweep_rate(wl, budget_s=15.0, n_cap=None):
     ea, eb = (int(x) for x in getattr(oracle_sweep_rate, "ess", "1/1").split("/"))
     s = oracle.Smc(kind, data, params, n, 12345)
     s.set_ess(ea, eb)
+    s.set_inplace(getattr(oracle_sweep_rate, "inplace", False))
     s.run()
     dt = time.perf_counter() - t0
     n = max(1000, int(n * budget_s / max(dt, 1e-3)))
@@ -181,6 +183,7 @@ def oracle_sweep_rate(wl, budget_s=15.0, n_cap=None):
     t0 = time.perf_counter()
     s = oracle.Smc(kind, data, params, n, 12345)
     s.set_ess(ea, eb)
+    s.set_inplace(getattr(oracle_sweep_rate, "inplace", False))
     s.run()
     dt = time.perf_counter() - t0
     st = s.stats()
@@ -237,7 +240,7 @@ def run_reference(args, wl):
 # ----------------------------------------------------------------------------- our arm
 def bench_sweeps(args, wl, smc, torch, world, rank):
     N = args.n or wl["n"]
-    model = model_for(smc, wl, args.rng)
+    model = model_for(smc, wl, args.rng, args.inplace)
     stream = torch.cuda.current_stream()
     if world == 1:
         h = smc.Smc(model, N, seed=1, stream=stream)
@@ -386,7 +389,10 @@ def bench_resample(args, wl, smc, torch):
     st_out = torch.empty_like(st_in)
     anc = torch.empty(n, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
-    r = smc.Resampler(n, S, seed=4, stream=stream)
+    r = smc.Resampler(n, S, seed=4, stream=stream, inplace=args.inplace)
+    if args.inplace:
+        del st_out
+        st_out = None                 # R-21: the state is updated in place
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
     for w in range(args.warmup):
         r.device(lw, st_in, st_out, anc, epoch=w)
@@ -473,16 +479,27 @@ def run_ours(args, wl):
         achieved = r["alg_bytes"] / (r["t_ms"] * 1e-3) / 1e9
         n, D = r["n"], r["D"]
         g_bytes = n * 12 + 64 * (D + n)          # anc_gather: lw read, anc write, states
+        kname = "anc_gather_kernel (ancestors + fused gather)"
+        metric = "resample effective HBM GB/s (B_alg = N*20 + 64*(D+N))"
+        if args.inplace:
+            # offspring: lw 8 + O_k 4; permute: O_k 4 + survivors' anc 4 D + hole/extra
+            # lists 8 H; fill: lists 8 H + anc 4 H + state 2*64 H   (H = N - D holes)
+            H = n - D
+            g_bytes = n * 16 + 4 * D + H * (20 + 2 * 64)
+            kname = "in-place chain (offspring + permute + fill_holes kernels, R-21)"
+            metric = ("resample effective GB/s, in place (B_alg of the out-of-place step, "
+                      "N*20 + 64*(D+N), per unit time)")
         g_ms = r["ms_kernel"][2]
         g_ach = g_bytes / (g_ms * 1e-3) / 1e9
-        tr = traffic(f"resample:{n}:anc_gather")
-        line = dict(metric="resample effective HBM GB/s (B_alg = N*20 + 64*(D+N))", value=achieved,
+        tr = None if args.inplace else traffic(f"resample:{n}:anc_gather")
+        line = dict(metric=metric, value=achieved,
                     unit="GB/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
                     ms_per_step=r["t_ms"], higher_is_better=True, scaling="weak", vs_baseline=None,
                     dtype="f64/u128", data="synthetic",
                     config=dict(workload="resample", desc=wl["desc"], n_per_gpu=r["n"],
-                                state_bytes=64, sigma=args.sigma, l2="flushed between steps"),
-                    roofline=dict(bound="hbm", kernel="anc_gather_kernel (ancestors + fused gather)",
+                                state_bytes=64, sigma=args.sigma, l2="flushed between steps",
+                                inplace=args.inplace),
+                    roofline=dict(bound="hbm", kernel=kname,
                                   achieved=g_ach, peak=hbm_peak, unit="GB/s", frac=g_ach / hbm_peak,
                                   traffic=(tr["bytes"] if tr else None),
                                   algorithmic_bytes=g_bytes, ms=g_ms, peak_source=pk_kind),
@@ -490,9 +507,10 @@ def run_ours(args, wl):
                                         frac=achieved / hbm_peak, algorithmic_bytes=r["alg_bytes"],
                                         note="max + reduce + anc_gather + finalize; B_alg excludes "
                                              "the standalone max pass (8 B/particle)"),
-                    kernel_ms=dict(zip(["max", "reduce", "anc_gather", "finalize"], r["ms_kernel"])),
+                    kernel_ms=dict(zip(["max", "reduce", "inplace_chain" if args.inplace else "anc_gather",
+                                        "finalize"], r["ms_kernel"])),
                     distinct_ancestors=D,
-                    gpu_launches=5 * args.steps, clocks=r["clocks"])
+                    gpu_launches=(7 if args.inplace else 5) * args.steps, clocks=r["clocks"])
         if rank == 0:
             print(json.dumps(line), flush=True)
         return
@@ -512,7 +530,7 @@ def run_ours(args, wl):
                 config=dict(workload=args.workload, desc=wl["desc"], n_per_gpu=N,
                             rng=("analytic (no side trees)" if wl.get("analytic") else
                                  args.rng if wl["model"] in ("crbd", "clads2") else "sequential"),
-                            ess_threshold=args.ess,
+                            ess_threshold=args.ess, inplace=args.inplace,
                             epochs_per_sweep=r["epochs"] // args.steps,
                             l2="flushed between steps (state fits L2 within a sweep)"),
                 sweeps_per_s=r["sweeps"], mean_log_z=r["logz"],
@@ -565,6 +583,8 @@ def main():
     ap.add_argument("--ess", default=None,
                     help="ESS-adaptive resampling threshold a/b (DESIGN R-19); 1/1 = every checkpoint "
                          "(default: the workload's, 1/1 unless stated)")
+    ap.add_argument("--inplace", action="store_true",
+                    help="in-place resampling by ancestor permutation (DESIGN R-21, SURVEY f3)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
@@ -578,6 +598,7 @@ def main():
         args.ess = wl.get("ess", "1/1")
     oracle_sweep_rate.rng = args.rng
     oracle_sweep_rate.ess = args.ess
+    oracle_sweep_rate.inplace = args.inplace
     if args.impl == "reference":
         run_reference(args, wl)
     else:

@@ -79,6 +79,15 @@ typedef enum {
  * trees are simulated).  CLADS2 with this flag: SMC_EINVAL (lineage-specific
  * rates have no closed-form E). */
 #define SMC_FLAG_ANALYTIC_UNDETECTED 4u
+/* Any kind: in-place resampling: the sorted
+ * systematic ancestors are permuted so that every particle with offspring
+ * keeps its slot and its extra copies fill the slots without offspring in
+ * ascending order; the state is updated in place (one state buffer, copies
+ * only into slots without offspring).  smc_ancestors returns the permuted
+ * ancestors.  Single shard only: smc_create_virtual with shards > 1 or
+ * smc_create_sharded with world > 1 -> SMC_EINVAL.  smc_resample_device:
+ * d_state_out must be NULL or equal to d_state_in. */
+#define SMC_FLAG_INPLACE 8u
 
 /*
  * Model description (all arrays COPIED at create).

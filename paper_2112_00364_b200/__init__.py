@@ -29,6 +29,7 @@ CRBD, CLADS2, SEIR, GEOMETRIC, SSM, CONSTW, RESAMPLE_BENCH = 1, 2, 3, 10, 11, 12
 FLAG_STRICT = 1
 FLAG_LINEAGE_RNG = 2
 FLAG_ANALYTIC_UNDETECTED = 4
+FLAG_INPLACE = 8
 
 FIELDS = {
     CRBD: ["pc", "branch", "lambda", "mu"],
@@ -173,28 +174,28 @@ class Model:
                      flags=flags | (FLAG_LINEAGE_RNG if lineage else 0) | (FLAG_ANALYTIC_UNDETECTED if analytic else 0))
 
     @staticmethod
-    def clads2(tree, params=(1.0, -1.0, -1.0, -1.0, -1.0), flags=0, lineage=False):
+    def clads2(tree, params=(1.0, -1.0, -1.0, -1.0, -1.0), flags=0, lineage=False):  # noqa: D401
         return Model(CLADS2, tree_data(tree), params, flags=flags | (FLAG_LINEAGE_RNG if lineage else 0))
 
     @staticmethod
-    def seir(y, params=None):
-        return Model(SEIR, np.asarray(y, dtype=np.float64), params)
+    def seir(y, params=None, flags=0):
+        return Model(SEIR, np.asarray(y, dtype=np.float64), params, flags=flags)
 
     @staticmethod
-    def ssm(y, params=(0.0, 100.0, 2.0, 1.0, 5.0)):
-        return Model(SSM, np.asarray(y, dtype=np.float64), params)
+    def ssm(y, params=(0.0, 100.0, 2.0, 1.0, 5.0), flags=0):
+        return Model(SSM, np.asarray(y, dtype=np.float64), params, flags=flags)
 
     @staticmethod
-    def geometric(p=0.5, w=1.5):
-        return Model(GEOMETRIC, None, (p, w))
+    def geometric(p=0.5, w=1.5, flags=0):
+        return Model(GEOMETRIC, None, (p, w), flags=flags)
 
     @staticmethod
-    def constw(logw=float(np.log(3.0)), K=1):
-        return Model(CONSTW, None, (logw, K))
+    def constw(logw=float(np.log(3.0)), K=1, flags=0):
+        return Model(CONSTW, None, (logw, K), flags=flags)
 
     @staticmethod
-    def resample_bench(state_bytes=64):
-        return Model(RESAMPLE_BENCH, None, None, state_bytes=state_bytes)
+    def resample_bench(state_bytes=64, flags=0):
+        return Model(RESAMPLE_BENCH, None, None, state_bytes=state_bytes, flags=flags)
 
 
 class Smc:
@@ -319,8 +320,10 @@ class Resampler:
     state_bytes each.  State buffers are SoA planes: plane p of particle k at
     byte (p * n + k) * 16."""
 
-    def __init__(self, n: int, state_bytes: int = 64, seed: int = 4, stream=None):
-        self.model = Model.resample_bench(state_bytes)
+    def __init__(self, n: int, state_bytes: int = 64, seed: int = 4, stream=None, inplace=False):
+        """inplace: permuted ancestors, state updated in place (DESIGN.md R-21);
+        then device() takes state_out=None (or the same buffer as state_in)."""
+        self.model = Model.resample_bench(state_bytes, FLAG_INPLACE if inplace else 0)
         self.h = _lib.smc_create(C.byref(self.model.c), int(n), int(seed))
         if not self.h:
             raise SmcError(EINVAL, _lib.smc_errmsg(None).decode())

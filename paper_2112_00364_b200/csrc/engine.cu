@@ -72,6 +72,7 @@ struct Shard {
   u128* tile_excl = nullptr;
   U192* tile_q2 = nullptr;
   Ctrl* ctrl = nullptr;
+  uint32_t* scratch = nullptr;     // in-place resampling (R-21): offs, hole_dst, extra_src, tile_nz[2]
   uint4** d_dst_planes[2] = {nullptr, nullptr};  // device arrays [world]
   uint32_t** d_dst_anc = nullptr;                 // device array [world]
 };
@@ -84,6 +85,7 @@ struct smc_ctx {
   int kind = 0;
   bool lineage = false;           // §R-18 lineage-keyed side trees (SMC_FLAG_LINEAGE_RNG)
   bool analytic = false;          // §R-20 CRBD with 2E(t) per hidden event (SMC_FLAG_ANALYTIC_UNDETECTED)
+  bool inplace = false;           // §R-21 permuted ancestors, one state buffer (SMC_FLAG_INPLACE)
   int lr_grid = 0;                // persistent grid of the cooperative kernel
   int prop_grid = 0;              // resident-CTA grid of propagate_kernel<M> (grid-stride)
   TaskArrays tasks{};
@@ -234,6 +236,7 @@ int setup_model(smc_ctx* h, const smc_model* m) {
   h->kind = m->kind;
   h->flags = m->flags;
   h->analytic = (m->flags & SMC_FLAG_ANALYTIC_UNDETECTED) != 0;
+  h->inplace = (m->flags & SMC_FLAG_INPLACE) != 0;
   if (h->analytic && m->kind != SMC_CRBD)
     return fail(h, SMC_EINVAL, "SMC_FLAG_ANALYTIC_UNDETECTED applies to SMC_CRBD only");
   h->lineage = !h->analytic && (m->flags & SMC_FLAG_LINEAGE_RNG) &&
@@ -317,12 +320,13 @@ int setup_model(smc_ctx* h, const smc_model* m) {
 int alloc_shard(smc_ctx* h, Shard& s) {
   const unsigned long long n = h->n_per;
   const size_t plane_bytes = (size_t)h->planes * n * 16;
-  const size_t anc_off = 2 * plane_bytes;
+  const size_t anc_off = (h->inplace ? 1 : 2) * plane_bytes;   // in place: one state buffer
   const size_t block = anc_off + n * sizeof(uint32_t);
   CU(cudaMalloc(&s.ipc_block, block));
   s.planes[0] = (uint4*)s.ipc_block;
-  s.planes[1] = (uint4*)(s.ipc_block + plane_bytes);
+  s.planes[1] = h->inplace ? s.planes[0] : (uint4*)(s.ipc_block + plane_bytes);
   s.anc = (uint32_t*)(s.ipc_block + anc_off);
+  if (h->inplace) CU(cudaMalloc(&s.scratch, (3 * n + 2 * (size_t)h->n_tiles) * sizeof(uint32_t)));
   CU(cudaMalloc(&s.lw, n * sizeof(double)));
   CU(cudaMalloc(&s.tile_sum, (size_t)h->n_tiles * sizeof(u128)));
   CU(cudaMalloc(&s.tile_excl, (size_t)h->n_tiles * sizeof(u128)));
@@ -444,6 +448,8 @@ int common_init(smc_ctx* h, const smc_model* m, unsigned long long n_per, int wo
     if (h->kind == SMC_CLADS2) CU(cudaMalloc(&h->tasks.lam, nt * sizeof(double)));
     CU(cudaMalloc(&h->tasks.owner, nt * sizeof(unsigned short)));
   }
+  if (h->inplace && world > 1)
+    return fail(h, SMC_EINVAL, "SMC_FLAG_INPLACE needs a single shard (no cross-shard hole matching yet)");
   h->shards.resize(n_local_shards);
   for (int i = 0; i < n_local_shards; ++i) {
     Shard& s = h->shards[i];
@@ -572,6 +578,12 @@ ResArgs res_args(smc_ctx* h, Shard& s, const double* lw, const uint4* src, int d
   a.dst_planes = s.d_dst_planes[dst_par];
   a.dst_anc = s.d_dst_anc;
   a.ctrl = s.ctrl;
+  const unsigned long long n = h->n_per;
+  a.offs = s.scratch;
+  a.hole_dst = s.scratch ? s.scratch + n : nullptr;
+  a.extra_src = s.scratch ? s.scratch + 2 * n : nullptr;
+  a.tile_nz = s.scratch ? s.scratch + 3 * n : nullptr;
+  a.tile_nz_excl = s.scratch ? s.scratch + 3 * n + h->n_tiles : nullptr;
   return a;
 }
 template <int IT>
@@ -589,6 +601,31 @@ void launch_anc_gather_it(smc_ctx* h, const ResArgs& a) {
 void launch_anc_gather(smc_ctx* h, const ResArgs& a) {
   if (h->items == kItemsSmall) launch_anc_gather_it<kItemsSmall>(h, a);
   else launch_anc_gather_it<kItems>(h, a);
+}
+// in-place chain (R-21): offspring, permute, fill holes
+void launch_inplace(smc_ctx* h, const ResArgs& a) {
+  const unsigned grid = (unsigned)h->n_tiles;
+  if (h->items == kItemsSmall) {
+    offspring_kernel<kItemsSmall><<<grid, kThreads, 0, h->stream>>>(a);
+    permute_kernel<kItemsSmall><<<grid, kThreads, 0, h->stream>>>(a);
+  } else {
+    offspring_kernel<kItems><<<grid, kThreads, 0, h->stream>>>(a);
+    permute_kernel<kItems><<<grid, kThreads, 0, h->stream>>>(a);
+  }
+  const unsigned fgrid = (unsigned)std::min<unsigned long long>((h->n_per + kThreads - 1) / kThreads, 148ull * 8);
+  switch (h->planes) {
+    case 1: fill_holes_kernel<1><<<fgrid, kThreads, 0, h->stream>>>(a); break;
+    case 2: fill_holes_kernel<2><<<fgrid, kThreads, 0, h->stream>>>(a); break;
+    case 4: fill_holes_kernel<4><<<fgrid, kThreads, 0, h->stream>>>(a); break;
+    case 6: fill_holes_kernel<6><<<fgrid, kThreads, 0, h->stream>>>(a); break;
+    case 8: fill_holes_kernel<8><<<fgrid, kThreads, 0, h->stream>>>(a); break;
+    default: fill_holes_kernel<0><<<fgrid, kThreads, 0, h->stream>>>(a); break;
+  }
+}
+// ancestors + state gather: the out-of-place fused kernel or the in-place chain
+void launch_resample_tail(smc_ctx* h, const ResArgs& a) {
+  if (h->inplace) launch_inplace(h, a);
+  else launch_anc_gather(h, a);
 }
 void launch_reduce(smc_ctx* h, const ResArgs& a) {
   const unsigned grid = (unsigned)((h->n_tiles + 1) / 2);     // two tiles per CTA
@@ -625,7 +662,7 @@ int enqueue_epoch(smc_ctx* h) {
   CU(cudaGetLastError());
   rc = allgather_rec(h, h->d_recB + cur * h->world, sizeof(RecB));
   if (rc) return rc;
-  for (auto& s : h->shards) launch_anc_gather(h, res_args(h, s, s.lw, s.planes[cur], cur ^ 1));
+  for (auto& s : h->shards) launch_resample_tail(h, res_args(h, s, s.lw, s.planes[cur], cur ^ 1));
   CU(cudaGetLastError());
   rc = barrier(h);
   if (rc) return rc;
@@ -864,6 +901,7 @@ void smc_destroy(smc_handle h) {
   for (auto& s : h->shards) {
     cudaFree(s.ipc_block); cudaFree(s.lw); cudaFree(s.tile_sum); cudaFree(s.tile_excl); cudaFree(s.tile_q2);
     cudaFree(s.ctrl); cudaFree(s.d_dst_planes[0]); cudaFree(s.d_dst_planes[1]); cudaFree(s.d_dst_anc);
+    cudaFree(s.scratch);
   }
   cudaFree(h->d_table); cudaFree(h->d_logfact); cudaFree(h->d_recA); cudaFree(h->d_recB); cudaFree(h->d_barrier);
   cudaFree(h->tasks.sid); cudaFree(h->tasks.lam); cudaFree(h->tasks.owner);
@@ -1114,7 +1152,10 @@ int smc_resample_device(smc_handle h, const double* d_lw, const void* d_state_in
                         uint32_t* d_anc, uint32_t epoch, double* logz_inc) {
   if (!h || h->kind != SMC_RESAMPLE_BENCH || h->shards.size() != 1 || h->world != 1)
     return fail(h, SMC_ESTATE, "smc_resample_device needs a single-shard RESAMPLE_BENCH handle");
+  if (h->inplace && !d_state_out) d_state_out = const_cast<void*>(d_state_in);
   if (!d_lw || !d_state_in || !d_state_out || !d_anc) return fail(h, SMC_EINVAL, "NULL buffer");
+  if (h->inplace && d_state_out != d_state_in)
+    return fail(h, SMC_EINVAL, "SMC_FLAG_INPLACE: d_state_out must be NULL or d_state_in");
   Shard& s = h->shards[0];
   // destination tables point at the caller's buffers
   uint4* dst = (uint4*)d_state_out;
@@ -1128,7 +1169,7 @@ int smc_resample_device(smc_handle h, const double* d_lw, const void* d_state_in
   ResArgs a = res_args(h, s, d_lw, (const uint4*)d_state_in, 1);
   launch_reduce(h, a);
   if (h->timing) CU(cudaEventRecord(h->rev[2], h->stream));
-  launch_anc_gather(h, a);
+  launch_resample_tail(h, a);
   if (h->timing) CU(cudaEventRecord(h->rev[3], h->stream));
   launch_finalize(h, s);
   if (h->timing) CU(cudaEventRecord(h->rev[4], h->stream));
@@ -1250,7 +1291,7 @@ int smc_resample_step(smc_handle h, uint32_t epoch) {
   for (auto& s : h->shards) launch_reduce(h, res_args(h, s, s.lw, s.planes[cur], cur ^ 1));
   rc = allgather_rec(h, h->d_recB + par * h->world, sizeof(RecB));
   if (rc) return rc;
-  for (auto& s : h->shards) launch_anc_gather(h, res_args(h, s, s.lw, s.planes[cur], cur ^ 1));
+  for (auto& s : h->shards) launch_resample_tail(h, res_args(h, s, s.lw, s.planes[cur], cur ^ 1));
   rc = barrier(h);
   if (rc) return rc;
   for (auto& s : h->shards) launch_finalize(h, s);

@@ -65,7 +65,7 @@ struct Ctrl {
   unsigned max_rounds;               // diag: longest cooperative phase (rounds) in a batch
   unsigned long long side_roots;     // diag: hidden events (side-tree roots) generated
   unsigned max_side_nodes;           // diag: largest per-particle side-tree node count
-  unsigned pad_;
+  unsigned holes;                    // in-place resampling (R-21): slots without offspring
 };
 
 enum { ST_OK = 0, ST_REJECTED = 4, ST_NAN = 5, ST_OVERFLOW = 6 };
@@ -391,6 +391,12 @@ struct ResArgs {
   uint4* const* dst_planes;           // [world] destination buffers (peer pointers)
   uint32_t* const* dst_anc;           // [world]
   Ctrl* ctrl;
+  // in-place resampling (R-21; single shard)
+  uint32_t* offs;                     // [n] O_k: output boundary after particle k
+  uint32_t* tile_nz;                  // [n_tiles] particles with offspring per tile
+  uint32_t* tile_nz_excl;             // [n_tiles] exclusive prefix of tile_nz
+  uint32_t* hole_dst;                 // [n] slot of the h-th particle without offspring
+  uint32_t* extra_src;                // [n] source of the h-th extra copy
 };
 
 struct Global {
@@ -682,6 +688,222 @@ __global__ void __launch_bounds__(kThreads) anc_gather_kernel(ResArgs a) {
     a.dst_anc[dshard][dl] = (uint32_t)(a.shard_base + src);
   }
   if (a.world > 1) __threadfence_system();   // peer stores visible before the epoch barrier
+}
+
+// ============================================================================
+// in-place resampling (single shard).  From
+// the sorted ancestors of the systematic grid: particles with offspring keep
+// their slot; their extra copies fill the slots without offspring in order.
+//   offspring_kernel  O_k per particle (stored), survivors per tile, last CTA:
+//                     tile prefix of survivors and the hole count H
+//   permute_kernel    anc[k] = k for survivors, hole list, extra-copy list
+//   fill_holes_kernel for h < H: anc[hole_h] = extra_h, copy the state planes
+//                     in place (holes are never sources)
+// ============================================================================
+__device__ __forceinline__ bool inplace_active(const ResArgs& a, unsigned epoch, Global& G) {
+  const unsigned par = epoch & 1;
+  G = read_global(a.recA + par * a.world, a.world);
+  if (!G.ok || G.alive == 0) return false;           // error, or final epoch: no resample
+  u128 W = 0;
+  for (int g = 0; g < a.world; ++g) W += a.recB[par * a.world + g].W;
+  return ess_resample(W, total_q2(a.recB + par * a.world, a.world), a.n_total, a.ctrl->ess_a,
+                      a.ctrl->ess_b);                 // ESS skip: state stays where it is
+}
+
+template <int ITEMS>
+__global__ void __launch_bounds__(kThreads) offspring_kernel(ResArgs a) {
+  constexpr int kTile = kThreads * ITEMS;
+  constexpr int kItems = ITEMS;
+  __shared__ double s_lw[kTile];
+  __shared__ unsigned s_O[kTile];
+  __shared__ u128 s_w[kThreads / 32];
+  __shared__ unsigned s_n[kThreads / 32];
+  __shared__ unsigned long long s_jlo;
+  __shared__ unsigned s_ticket;
+  if (*(volatile unsigned*)&a.ctrl->done) return;
+  const unsigned epoch = a.ctrl->epoch;
+  Global G;
+  if (!inplace_active(a, epoch, G)) return;
+  u128 prefix;
+  const Grid gr = make_grid(a, a.recB + (epoch & 1) * a.world, epoch, prefix);
+  const unsigned long long base = (unsigned long long)blockIdx.x * kTile;
+  const int cnt = (int)min((unsigned long long)kTile, a.n_local - base);
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const int k = r * kThreads + threadIdx.x;
+    s_lw[k] = k < cnt ? __ldg(a.lw + base + k) : -INFINITY;
+  }
+  __syncthreads();
+  unsigned long long q[kItems];
+  u128 tsum = 0;
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    q[r] = quantize(s_lw[threadIdx.x * kItems + r], G.m);
+    tsum += q[r];
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  u128 incl = tsum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const u128 o = shfl_up_u128(incl, d);
+    if (lane >= d) incl += o;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  u128 woff = 0;
+  for (int w = 0; w < warp; ++w) woff += s_w[w];
+  const u128 tile_start = prefix + a.tile_excl[blockIdx.x];
+  u128 C = tile_start + woff + incl - tsum;
+  if (threadIdx.x == 0) s_jlo = gr.count_below(tile_start);
+  unsigned long long prevO = 0;
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    C += q[r];
+    const unsigned long long O = (q[r] == 0 && r > 0) ? prevO : gr.count_below(C);
+    s_O[threadIdx.x * kItems + r] = (unsigned)O;
+    prevO = O;
+  }
+  __syncthreads();
+  const unsigned jlo = (unsigned)s_jlo;
+  unsigned nz = 0;
+  for (int k = threadIdx.x; k < cnt; k += kThreads) {     // striped: coalesced store
+    const unsigned O = s_O[k];
+    a.offs[base + k] = O;
+    nz += O > (k ? s_O[k - 1] : jlo);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) nz += __shfl_xor_sync(0xffffffffu, nz, d);
+  if (lane == 0) s_n[warp] = nz;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int w = 0; w < kThreads / 32; ++w) t += s_n[w];
+    a.tile_nz[blockIdx.x] = t;
+    if (t) atomicAdd(&a.ctrl->distinct, (unsigned long long)t);
+    __threadfence();
+    s_ticket = atomicAdd(&a.ctrl->counter, 1u);
+  }
+  __syncthreads();
+  if (s_ticket != gridDim.x - 1) return;
+  // ---- last CTA: exclusive scan of the per-tile survivor counts
+  __threadfence();
+  const int nt = a.n_tiles;
+  const int per = (nt + kThreads - 1) / kThreads;
+  const int lo = threadIdx.x * per, hi = min(nt, lo + per);
+  unsigned local = 0;
+  for (int t = lo; t < hi; ++t) local += __ldcg(a.tile_nz + t);
+  unsigned inc2 = local;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned o = __shfl_up_sync(0xffffffffu, inc2, d);
+    if (lane >= d) inc2 += o;
+  }
+  __syncthreads();                                       // s_n reused
+  if (lane == 31) s_n[warp] = inc2;
+  __syncthreads();
+  unsigned wo = 0;
+  for (int w = 0; w < warp; ++w) wo += s_n[w];
+  unsigned run = wo + inc2 - local;
+  for (int t = lo; t < hi; ++t) {
+    a.tile_nz_excl[t] = run;
+    run += __ldcg(a.tile_nz + t);
+  }
+  if (threadIdx.x == kThreads - 1) {
+    a.ctrl->holes = (unsigned)(a.n_local - run);        // run = survivors (distinct ancestors)
+    a.ctrl->counter = 0;
+  }
+}
+
+template <int ITEMS>
+__global__ void __launch_bounds__(kThreads) permute_kernel(ResArgs a) {
+  constexpr int kTile = kThreads * ITEMS;
+  constexpr int kItems = ITEMS;
+  __shared__ unsigned s_O[kTile];
+  __shared__ unsigned s_E[kTile];
+  __shared__ unsigned s_n[kThreads / 32];
+  __shared__ unsigned s_prev;
+  if (*(volatile unsigned*)&a.ctrl->done) return;
+  Global G;
+  if (!inplace_active(a, a.ctrl->epoch, G)) return;
+  const unsigned long long base = (unsigned long long)blockIdx.x * kTile;
+  const int cnt = (int)min((unsigned long long)kTile, a.n_local - base);
+  for (int k = threadIdx.x; k < cnt; k += kThreads) s_O[k] = a.offs[base + k];
+  if (threadIdx.x == 0) s_prev = base ? a.offs[base - 1] : 0u;    // O_{-1} = 0 (single shard)
+  __syncthreads();
+  // survivors before each item: blocked per thread, CTA scan, tile prefix
+  const unsigned prev0 = s_prev;
+  unsigned c = 0;
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const int k = threadIdx.x * kItems + r;
+    if (k < cnt) c += s_O[k] > (k ? s_O[k - 1] : prev0);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned incl = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned o = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += o;
+  }
+  if (lane == 31) s_n[warp] = incl;
+  __syncthreads();
+  unsigned wo = 0;
+  for (int w = 0; w < warp; ++w) wo += s_n[w];
+  const unsigned tile_d = a.tile_nz_excl[blockIdx.x];
+  unsigned D = tile_d + wo + incl - c;                  // survivors before this thread's first item
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const int k = threadIdx.x * kItems + r;
+    if (k < cnt) {
+      D += s_O[k] > (k ? s_O[k - 1] : prev0);
+      s_E[k] = s_O[k] - D;                               // extra copies through particle k
+    }
+  }
+  __syncthreads();
+  uint32_t* anc = a.dst_anc[a.rank];
+  for (int k = threadIdx.x; k < cnt; k += kThreads) {   // striped: coalesced anc stores
+    const unsigned O = s_O[k];
+    const unsigned gk = (unsigned)(a.shard_base + base + k);
+    if (O > (k ? s_O[k - 1] : prev0)) anc[base + k] = gk;     // survivor keeps its slot
+    else a.hole_dst[(base + k) - (O - s_E[k])] = gk;          // rank among the holes
+  }
+  // extra copies of this tile: ranks [E_{base-1}, E_{last}); rank e belongs to
+  // the first item with s_E > e
+  const unsigned elo = prev0 - tile_d, ehi = cnt > 0 ? s_E[cnt - 1] : elo;
+  for (unsigned e = elo + threadIdx.x; e < ehi; e += kThreads) {
+    int lo = 0, hi = cnt - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (s_E[mid] > e) hi = mid; else lo = mid + 1;
+    }
+    a.extra_src[e] = (unsigned)(a.shard_base + base + lo);
+  }
+}
+
+template <int P>   // P = planes per particle (<= 0: runtime a.planes)
+__global__ void __launch_bounds__(kThreads) fill_holes_kernel(ResArgs a) {
+  if (*(volatile unsigned*)&a.ctrl->done) return;
+  Global G;
+  if (!inplace_active(a, a.ctrl->epoch, G)) return;
+  const unsigned H = a.ctrl->holes;
+  uint4* pl = const_cast<uint4*>(a.src_planes);          // the one state buffer
+  uint32_t* anc = a.dst_anc[a.rank];
+  const int np = P > 0 ? P : a.planes;
+  for (unsigned long long h = (unsigned long long)blockIdx.x * kThreads + threadIdx.x; h < H;
+       h += (unsigned long long)gridDim.x * kThreads) {
+    const unsigned dst = a.hole_dst[h], src = a.extra_src[h];
+    anc[dst] = src;
+    if (P > 0) {
+      uint4 v[P > 0 ? P : 1];
+#pragma unroll
+      for (int p = 0; p < (P > 0 ? P : 1); ++p) v[p] = __ldg(pl + (unsigned long long)p * a.n_local + src);
+#pragma unroll
+      for (int p = 0; p < (P > 0 ? P : 1); ++p) pl[(unsigned long long)p * a.n_local + dst] = v[p];
+    } else {
+      for (int p = 0; p < np; ++p)
+        pl[(unsigned long long)p * a.n_local + dst] = __ldg(pl + (unsigned long long)p * a.n_local + src);
+    }
+  }
 }
 
 // ============================================================================

@@ -16,15 +16,16 @@ ap.add_argument("--workload", default="crbd")
 ap.add_argument("--n", type=int, default=1_000_000)
 ap.add_argument("--sweeps", type=int, default=1)
 ap.add_argument("--rng", default="lineage")
+ap.add_argument("--inplace", action="store_true")
 args = ap.parse_args()
 if args.workload == "resample":
     n = args.n
     dev = torch.device("cuda")
     lw = torch.randn(n, device=dev, dtype=torch.float64)
     st = torch.randint(0, 1 << 30, (16 * n,), device=dev, dtype=torch.int32)
-    out = torch.empty_like(st)
+    out = None if args.inplace else torch.empty_like(st)
     anc = torch.empty(n, device=dev, dtype=torch.int32)
-    r = smc.Resampler(n, 64, 4)
+    r = smc.Resampler(n, 64, 4, inplace=args.inplace)
     for e in range(1 + args.sweeps):
         r.device(lw, st, out, anc, epoch=e)
     torch.cuda.synchronize()
