@@ -383,10 +383,13 @@ struct Clads2Model {
     double pend[PEND] = {0, 0, 0, 0, 0, 0};
   };
   static const int NF = 7 + PEND;
+  // The pending-rate stack holds pend[0 .. sp); entries at or above the stack
+  // pointer are not part of the state (the unused part of the stack
+  // beyond the stack pointer is not copied) and read as 0.
   void fields(const State& s, double* f) const {
     f[0] = s.pc; f[1] = s.branch; f[2] = s.sp; f[3] = s.sigma; f[4] = s.alpha;
     f[5] = s.eps; f[6] = s.lam;
-    for (int i = 0; i < PEND; ++i) f[7 + i] = s.pend[i];
+    for (int i = 0; i < PEND; ++i) f[7 + i] = i < s.sp ? s.pend[i] : 0.0;
   }
   static bool bad_rate(double r) { return !(r <= CLADS2_MAX_RATE); }
   double daughter(const State& s, double lam, double z) const {
