@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -86,6 +87,7 @@ struct smc_ctx {
   bool lineage = false;           // §R-18 lineage-keyed side trees (SMC_FLAG_LINEAGE_RNG)
   bool analytic = false;          // §R-20 CRBD with 2E(t) per hidden event (SMC_FLAG_ANALYTIC_UNDETECTED)
   bool inplace = false;           // §R-21 permuted ancestors, one state buffer (SMC_FLAG_INPLACE)
+  bool stack_prefix = true;       // §R-22 copy only the used stack prefix (env SMC_NO_STACK_PREFIX=1: off, diagnostics)
   int lr_grid = 0;                // persistent grid of the cooperative kernel
   int prop_grid = 0;              // resident-CTA grid of propagate_kernel<M> (grid-stride)
   TaskArrays tasks{};
@@ -237,6 +239,10 @@ int setup_model(smc_ctx* h, const smc_model* m) {
   h->flags = m->flags;
   h->analytic = (m->flags & SMC_FLAG_ANALYTIC_UNDETECTED) != 0;
   h->inplace = (m->flags & SMC_FLAG_INPLACE) != 0;
+  {
+    const char* e = std::getenv("SMC_NO_STACK_PREFIX");
+    h->stack_prefix = !(e && e[0] == '1');
+  }
   if (h->analytic && m->kind != SMC_CRBD)
     return fail(h, SMC_EINVAL, "SMC_FLAG_ANALYTIC_UNDETECTED applies to SMC_CRBD only");
   h->lineage = !h->analytic && (m->flags & SMC_FLAG_LINEAGE_RNG) &&
@@ -584,6 +590,10 @@ ResArgs res_args(smc_ctx* h, Shard& s, const double* lw, const uint4* src, int d
   a.extra_src = s.scratch ? s.scratch + 2 * n : nullptr;
   a.tile_nz = s.scratch ? s.scratch + 3 * n : nullptr;
   a.tile_nz_excl = s.scratch ? s.scratch + 3 * n + h->n_tiles : nullptr;
+  a.stk0 = a.stk_n = a.stk_per = a.sp_word = 0;
+  if (h->kind == SMC_CLADS2 && h->stack_prefix) {   // R-22: pending-rate stack, planes 2..4, sp = P5.z
+    a.stk0 = 2; a.stk_n = 3; a.stk_per = 2; a.sp_word = 22;
+  }
   return a;
 }
 template <int IT>
@@ -763,9 +773,9 @@ void decode(int kind, const uint32_t* w, double* f) {
   switch (kind) {
     case SMC_CRBD:
       f[0] = i(4); f[1] = i(5); f[2] = d(0); f[3] = d(2); break;
-    case SMC_CLADS2:
+    case SMC_CLADS2:   // stack entries at or above sp are not state (R-22): 0
       f[0] = i(20); f[1] = i(21); f[2] = i(22); f[3] = d(0); f[4] = d(2); f[5] = d(4); f[6] = d(6);
-      for (int k = 0; k < 6; ++k) f[7 + k] = d(8 + 2 * k);
+      for (int k = 0; k < 6; ++k) f[7 + k] = k < (int)w[22] ? d(8 + 2 * k) : 0.0;
       break;
     case SMC_SEIR:
       f[0] = i(20); f[1] = i(19); f[2] = d(0); f[3] = d(2); f[4] = d(4); f[5] = d(6); f[6] = d(8);

@@ -397,7 +397,25 @@ struct ResArgs {
   uint32_t* tile_nz_excl;             // [n_tiles] exclusive prefix of tile_nz
   uint32_t* hole_dst;                 // [n] slot of the h-th particle without offspring
   uint32_t* extra_src;                // [n] source of the h-th extra copy
+  // stack-prefix copy (R-22): planes [stk0, stk0 + stk_n) hold a stack of
+  // stk_per entries per plane whose pointer is word sp_word of the particle's
+  // planes; only the first ceil(sp / stk_per) stack planes are copied
+  int stk0, stk_n, stk_per, sp_word;
 };
+
+// First stack plane of particle `src` that need not be copied (planes
+// [skip_lo, stk0 + stk_n) are beyond the stack pointer); a.stk_n == 0: none.
+__device__ __forceinline__ int stack_skip_lo(const ResArgs& a, const uint4* planes, unsigned long long src) {
+  if (a.stk_n == 0) return 1 << 30;
+  const uint4 w = __ldg(planes + (unsigned long long)(a.sp_word >> 2) * a.n_local + src);
+  const int c = a.sp_word & 3;
+  const unsigned sp = c == 0 ? w.x : c == 1 ? w.y : c == 2 ? w.z : w.w;
+  const int need = (int)min((unsigned)a.stk_n, (sp + (unsigned)a.stk_per - 1u) / (unsigned)a.stk_per);
+  return a.stk0 + need;
+}
+__device__ __forceinline__ bool copy_plane(const ResArgs& a, int p, int skip_lo) {
+  return p < skip_lo || p >= a.stk0 + a.stk_n;
+}
 
 struct Global {
   double m;
@@ -605,10 +623,13 @@ __global__ void __launch_bounds__(kThreads) anc_gather_kernel(ResArgs a) {
     // buffer so the epoch's buffer parity holds), ancestors unchanged
     uint4* dst = a.dst_planes[a.rank];
     const int np = P > 0 ? P : a.planes;
-    for (int k = threadIdx.x; k < cnt; k += kThreads)
+    for (int k = threadIdx.x; k < cnt; k += kThreads) {
+      const int lo = stack_skip_lo(a, a.src_planes, base + k);
       for (int p = 0; p < np; ++p)
-        dst[(unsigned long long)p * a.n_local + base + k] =
-            __ldg(a.src_planes + (unsigned long long)p * a.n_local + base + k);
+        if (copy_plane(a, p, lo))
+          dst[(unsigned long long)p * a.n_local + base + k] =
+              __ldg(a.src_planes + (unsigned long long)p * a.n_local + base + k);
+    }
     return;
   }
   // striped (coalesced) load, blocked use
@@ -675,15 +696,19 @@ __global__ void __launch_bounds__(kThreads) anc_gather_kernel(ResArgs a) {
     const unsigned long long dshard = j / a.n_local;
     const unsigned long long dl = j - dshard * a.n_local;
     uint4* dst = a.dst_planes[dshard];
+    const int skip = stack_skip_lo(a, a.src_planes, src);     // R-22: stack prefix only
     if (P > 0) {
       uint4 v[P > 0 ? P : 1];
 #pragma unroll
-      for (int p = 0; p < (P > 0 ? P : 1); ++p) v[p] = __ldg(a.src_planes + (unsigned long long)p * a.n_local + src);
+      for (int p = 0; p < (P > 0 ? P : 1); ++p)
+        if (copy_plane(a, p, skip)) v[p] = __ldg(a.src_planes + (unsigned long long)p * a.n_local + src);
 #pragma unroll
-      for (int p = 0; p < (P > 0 ? P : 1); ++p) dst[(unsigned long long)p * a.n_local + dl] = v[p];
+      for (int p = 0; p < (P > 0 ? P : 1); ++p)
+        if (copy_plane(a, p, skip)) dst[(unsigned long long)p * a.n_local + dl] = v[p];
     } else {
       for (int p = 0; p < np; ++p)
-        dst[(unsigned long long)p * a.n_local + dl] = __ldg(a.src_planes + (unsigned long long)p * a.n_local + src);
+        if (copy_plane(a, p, skip))
+          dst[(unsigned long long)p * a.n_local + dl] = __ldg(a.src_planes + (unsigned long long)p * a.n_local + src);
     }
     a.dst_anc[dshard][dl] = (uint32_t)(a.shard_base + src);
   }
@@ -893,15 +918,19 @@ __global__ void __launch_bounds__(kThreads) fill_holes_kernel(ResArgs a) {
        h += (unsigned long long)gridDim.x * kThreads) {
     const unsigned dst = a.hole_dst[h], src = a.extra_src[h];
     anc[dst] = src;
+    const int lo = stack_skip_lo(a, pl, src);               // R-22: stack prefix only
     if (P > 0) {
       uint4 v[P > 0 ? P : 1];
 #pragma unroll
-      for (int p = 0; p < (P > 0 ? P : 1); ++p) v[p] = __ldg(pl + (unsigned long long)p * a.n_local + src);
+      for (int p = 0; p < (P > 0 ? P : 1); ++p)
+        if (copy_plane(a, p, lo)) v[p] = __ldg(pl + (unsigned long long)p * a.n_local + src);
 #pragma unroll
-      for (int p = 0; p < (P > 0 ? P : 1); ++p) pl[(unsigned long long)p * a.n_local + dst] = v[p];
+      for (int p = 0; p < (P > 0 ? P : 1); ++p)
+        if (copy_plane(a, p, lo)) pl[(unsigned long long)p * a.n_local + dst] = v[p];
     } else {
       for (int p = 0; p < np; ++p)
-        pl[(unsigned long long)p * a.n_local + dst] = __ldg(pl + (unsigned long long)p * a.n_local + src);
+        if (copy_plane(a, p, lo))
+          pl[(unsigned long long)p * a.n_local + dst] = __ldg(pl + (unsigned long long)p * a.n_local + src);
     }
   }
 }
