@@ -446,7 +446,7 @@ int common_init(smc_ctx* h, const smc_model* m, unsigned long long n_per, int wo
     int dev = 0, sms = 0;
     CU(cudaGetDevice(&dev));
     CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const unsigned long long batches = (n_per + kLRThreads - 1) / kLRThreads;
+    const unsigned long long batches = (n_per + kOwners - 1) / kOwners;
     h->lr_grid = (int)std::min<unsigned long long>(batches, (unsigned long long)std::max(1, per_sm) * sms);
     h->tasks.cap = kTasksPerCta;
     const size_t nt = (size_t)h->lr_grid * h->tasks.cap;
@@ -543,7 +543,7 @@ void launch_prop_lr(smc_ctx* h, Shard& s, int cur) {
   a.p.rank = s.id;
   a.p.ctrl = s.ctrl;
   a.t = h->tasks;
-  a.n_batches = (unsigned)((h->n_per + kLRThreads - 1) / kLRThreads);
+  a.n_batches = (unsigned)((h->n_per + kOwners - 1) / kOwners);
   propagate_lr_kernel<M><<<h->lr_grid, kLRThreads, 0, h->stream>>>(a, h->mc);
 }
 void launch_propagate(smc_ctx* h, Shard& s, int cur) {

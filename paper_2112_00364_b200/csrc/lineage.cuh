@@ -36,11 +36,16 @@ namespace smc {
 #ifndef SMC_LR_MINB
 #define SMC_LR_MINB 8
 #endif
-constexpr int kLRThreads = SMC_LR_THREADS;     // particles (owners) per batch = threads per CTA
+#ifndef SMC_LR_OPT
+#define SMC_LR_OPT 1
+#endif
+constexpr int kLRThreads = SMC_LR_THREADS;     // threads per CTA = lanes per cooperative round
+constexpr int kOPT = SMC_LR_OPT;                 // particles (owners) per thread
+constexpr int kOwners = kLRThreads * kOPT;       // particles per batch
 constexpr unsigned kSideNodeCap = 1u << 22;      // nodes per branch (all its side trees)
-constexpr int kSeg = 512;                        // per-owner LIFO segment (tasks)
+constexpr int kSeg = 512 / kOPT;                 // per-owner LIFO segment (tasks)
 constexpr int kOverflowCap = 1 << 17;            // CTA-wide overflow LIFO (tasks)
-constexpr unsigned kTasksPerCta = (unsigned)(kLRThreads * kSeg + kOverflowCap);
+constexpr unsigned kTasksPerCta = (unsigned)(kOwners * kSeg + kOverflowCap);
 constexpr unsigned kTagNode = 3u, kTagChild = 4u, kTagZ = 5u;
 
 struct TaskArrays {
@@ -243,14 +248,14 @@ struct Clads2LR {
 // ---------------------------------------------------------------------------
 template <class M>
 __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kernel(LRArgs a, ModelConst C) {
-  __shared__ int s_cnt[kLRThreads];          // tasks in owner o's segment
+  __shared__ int s_cnt[kOwners];             // tasks in owner o's segment
   __shared__ int s_sel[kLRThreads];          // this round: lane -> task slot (owner-written)
   __shared__ int s_ovtop;                     // overflow stack top
   __shared__ int s_wsum[kLRThreads / 32];
   __shared__ unsigned s_batch;
-  __shared__ int s_dead[kLRThreads];          // 0 alive, 1 detected/rejected, 2 node cap
-  __shared__ unsigned s_nodes[kLRThreads];
-  __shared__ typename M::Owner s_own[kLRThreads];
+  __shared__ int s_dead[kOwners];             // 0 alive, 1 detected/rejected, 2 node cap
+  __shared__ unsigned s_nodes[kOwners];
+  __shared__ typename M::Owner s_own[kOwners];
   __shared__ int s_taskcap;
   __shared__ long long s_key[kLRThreads / 32];
   __shared__ unsigned long long s_acc[3][kLRThreads / 32];
@@ -258,23 +263,25 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
   if (*(volatile unsigned*)&p.ctrl->done) return;
   const unsigned epoch = p.ctrl->epoch;
   const unsigned long long seed = p.ctrl->seed;
+  const bool carry = p.ctrl->carry != 0;
   const double rho = C.p[0];
   const int tid = threadIdx.x;
   const unsigned long long tbase = (unsigned long long)blockIdx.x * kTasksPerCta;
   double2* T_sid = a.t.sid + tbase;
   double* T_lam = M::kHasLam ? a.t.lam + tbase : nullptr;
   unsigned short* T_own = a.t.owner + tbase;
+  constexpr unsigned long long kSegSlots = (unsigned long long)kOwners * kSeg;
   if (tid == 0) s_taskcap = 0;
   // store a task at a CTA-local slot; segment slots imply their owner
   auto put = [&](unsigned long long slot, int o, double s0, double lam0, unsigned long long id) {
     T_sid[slot] = make_double2(s0, __longlong_as_double((long long)id));
     if (M::kHasLam) T_lam[slot] = lam0;
-    if (slot >= (unsigned long long)kLRThreads * kSeg) T_own[slot] = (unsigned short)o;
+    if (slot >= kSegSlots) T_own[slot] = (unsigned short)o;
   };
   auto overflow_slot = [&]() -> long long {
     const int q = atomicAdd(&s_ovtop, 1);
     if (q >= kOverflowCap) { s_taskcap = 1; return -1; }
-    return (long long)kLRThreads * kSeg + q;
+    return (long long)kSegSlots + q;
   };
   // push one task for owner o: its segment, else the overflow stack
   auto push_task = [&](int o, double s0, double lam0, unsigned long long id) {
@@ -296,53 +303,89 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
   unsigned long long n_end = 0, n_start = 0, drw = 0, ovf = 0, roots = 0;
   bool bad = false;
   unsigned max_rounds = 0, max_nodes = 0;
+  const int warp_id = tid >> 5, lane_id = tid & 31;
 
   for (;;) {
     if (tid == 0) {
       s_batch = atomicAdd(&p.ctrl->batch, 1u);
       s_ovtop = 0;
     }
-    s_cnt[tid] = 0;
-    s_dead[tid] = 0;
-    s_nodes[tid] = 0;
+#pragma unroll
+    for (int q = 0; q < kOPT; ++q) {
+      s_cnt[q * kLRThreads + tid] = 0;
+      s_dead[q * kLRThreads + tid] = 0;
+      s_nodes[q * kLRThreads + tid] = 0;
+    }
     __syncthreads();
     const unsigned batch = s_batch;
     if (batch >= a.n_batches) break;
-    const unsigned long long i = (unsigned long long)batch * kLRThreads + tid;
-    const bool valid = i < p.n_local;
-    const uint32_t n_glob = (uint32_t)(p.shard_base + i);
-    // ---------------- phase 1: the particle's own stream
-    typename M::State st;
-    double lw = (valid && p.ctrl->carry) ? p.lw[i] : 0.0;   // R-19 carried weights
-    int K = 0;
-    bool active = false;
-    if (valid) {
-      M::load(st, p.planes, p.n_local, i);
-      if (M::pc(st) != kStop) {
-        active = true;
-        ++n_start;
-        Rng r(seed, n_glob, epoch);
-        auto push = [&](double s0, double lam0, unsigned k) { push_task(tid, s0, lam0, root_id(k)); };
-        if (!M::main_part(st, lw, r, C, s_own[tid], K, push)) s_dead[tid] = 1;
-        roots += (unsigned long long)K;
-        drw += 2ull * r.blk - (r.has_spare ? 1ull : 0ull);
+    const unsigned long long bbase = (unsigned long long)batch * kOwners;
+    // ---------------- phase 1: each particle's own stream; thread tid runs
+    // owners q*kLRThreads + tid (coalesced), stores the state at once and
+    // keeps lw, K and flags for phase 3
+    double lw[kOPT];
+    int K[kOPT];
+    bool act[kOPT], alive_end[kOPT];
+#pragma unroll
+    for (int q = 0; q < kOPT; ++q) {
+      const int o = q * kLRThreads + tid;
+      const unsigned long long i = bbase + o;
+      const bool valid = i < p.n_local;
+      lw[q] = (valid && carry) ? p.lw[i] : 0.0;   // R-19 carried weights
+      K[q] = 0;
+      act[q] = false;
+      alive_end[q] = false;
+      if (valid) {
+        typename M::State st;
+        M::load(st, p.planes, p.n_local, i);
+        if (M::pc(st) != kStop) {
+          act[q] = true;
+          ++n_start;
+          Rng r(seed, (uint32_t)(p.shard_base + i), epoch);
+          int k = 0;
+          auto push = [&](double s0, double lam0, unsigned kk) { push_task(o, s0, lam0, root_id(kk)); };
+          if (!M::main_part(st, lw[q], r, C, s_own[o], k, push)) s_dead[o] = 1;
+          K[q] = k;
+          roots += (unsigned long long)k;
+          drw += 2ull * r.blk - (r.has_spare ? 1ull : 0ull);
+          M::store(st, p.planes, p.n_local, i);
+        }
+        alive_end[q] = M::pc(st) != kStop;
       }
     }
-    __syncwarp();   // bar.red needs a converged warp (synccheck)
-    int n_act = __syncthreads_count(s_cnt[tid] > 0);
-    if (s_cnt[tid] > kSeg) s_cnt[tid] = kSeg;     // pushes beyond the segment went to overflow
-    // ---------------- phase 2: cooperative side-tree evaluation
-    // Four barriers per round: (A) scan + active count, (B) lane map written,
-    // (C) task records read, (D) pushes done.  The fair share W uses the
-    // previous round's active-owner count; each owner trims its share to the
-    // lanes left at its prefix offset, so at most kLRThreads tasks are taken.
+    __syncthreads();
+    // ---------------- phase 2: cooperative side-tree evaluation.  Thread tid
+    // manages owners kOPT*tid + q.  Four barriers per round: (A) scan, (B) lane
+    // map written, (C) task records read, (D) pushes done.  The fair share W
+    // uses the previous round's active-owner count; each owner trims its share
+    // to the lanes left at its prefix offset, so at most kLRThreads tasks are
+    // taken.  Task count and active-owner count travel packed in one scan.
+    int n_act = 0;
+    {
+      int c0 = 0;
+#pragma unroll
+      for (int q = 0; q < kOPT; ++q) {
+        const int o = kOPT * tid + q;
+        const int c = s_cnt[o];
+        if (c > kSeg) s_cnt[o] = kSeg;          // pushes beyond the segment went to overflow
+        c0 += c > 0;
+      }
+      n_act = __syncthreads_count(c0 > 0) * kOPT;   // estimate for the first round's share
+    }
     unsigned rounds = 0;
-    const int warp_id = tid >> 5, lane_id = tid & 31;
     for (;;) {
-      const int c = s_cnt[tid];
-      const int W = max(1, kLRThreads / max(1, n_act));
-      const int m = min(c, W);
-      int incl = m;
+      int c[kOPT], m[kOPT];
+      // lanes per owner: a heuristic (no result depends on it)
+      const int W = max(1, __float2int_rz((float)kLRThreads * __frcp_rn((float)max(1, n_act)) + 1e-3f));
+      int msum = 0, nact = 0;
+#pragma unroll
+      for (int q = 0; q < kOPT; ++q) {
+        c[q] = s_cnt[kOPT * tid + q];
+        m[q] = min(c[q], W);
+        msum += m[q];
+        nact += c[q] > 0;
+      }
+      int incl = msum | (nact << 16);          // msum <= kOPT * kLRThreads < 2^16
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const int o = __shfl_up_sync(0xffffffffu, incl, d);
@@ -350,29 +393,34 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
       }
       if (lane_id == 31) s_wsum[warp_id] = incl;
       const int ov = min(*(volatile int*)&s_ovtop, kOverflowCap);
-      __syncwarp();   // bar.red needs a converged warp (synccheck)
-      n_act = __syncthreads_count(c > 0);                                  // (A)
-      if (n_act == 0 && ov == 0) break;
-      int woff = 0, T = 0;
+      __syncthreads();                                                     // (A)
+      int woff = 0, tot = 0;
 #pragma unroll
       for (int w = 0; w < kLRThreads / 32; ++w) {
         const int v = s_wsum[w];
-        woff += w < warp_id ? v : 0;
-        T += v;
+        woff += w < warp_id ? (v & 0xFFFF) : 0;
+        tot += v;
       }
-      T = min(T, kLRThreads);
+      n_act = tot >> 16;
+      if (n_act == 0 && ov == 0) break;
+      const int T = min(tot & 0xFFFF, kLRThreads);
       {
-        // owner tid writes the slots of its top m tasks to lanes [off, off+m)
-        const int off = woff + incl - m;
-        const int me = max(0, min(m, kLRThreads - off));
-        const int seg = tid * kSeg;
-        for (int j = 0; j < me; ++j) s_sel[off + j] = seg + (c - 1 - j);
-        s_cnt[tid] = c - me;
-        // side-tree node count of the branch: every popped task of a live owner
-        // is evaluated this round (exact for the node-cap rule, no atomics)
-        if (me && s_dead[tid] == 0) {
-          s_nodes[tid] += (unsigned)me;
-          if (s_nodes[tid] > kSideNodeCap) atomicCAS(&s_dead[tid], 0, 2);
+        // owners write the slots of their top m tasks to lanes [off, off+m)
+        int off = woff + (incl & 0xFFFF) - msum;
+#pragma unroll
+        for (int q = 0; q < kOPT; ++q) {
+          const int o = kOPT * tid + q;
+          const int me = max(0, min(m[q], kLRThreads - off));
+          const int seg = o * kSeg;
+          for (int j = 0; j < me; ++j) s_sel[off + j] = seg + (c[q] - 1 - j);
+          s_cnt[o] = c[q] - me;
+          // side-tree node count of the branch: every popped task of a live
+          // owner is evaluated this round (exact for the node-cap rule)
+          if (me && s_dead[o] == 0) {
+            s_nodes[o] += (unsigned)me;
+            if (s_nodes[o] > kSideNodeCap) atomicCAS(&s_dead[o], 0, 2);
+          }
+          off += m[q];
         }
         if (tid == 0) s_ovtop = ov - min(ov, kLRThreads - T);
       }
@@ -387,7 +435,7 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
         slot = (unsigned long long)s_sel[tid];
         have = true;
       } else if (tid - T < ov) {
-        slot = (unsigned long long)kLRThreads * kSeg + (ov - 1 - (tid - T));
+        slot = kSegSlots + (ov - 1 - (tid - T));
         have = true;
       }
       if (have) {
@@ -395,13 +443,13 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
         ts = rec.x;
         tidv = (unsigned long long)__double_as_longlong(rec.y);
         if (M::kHasLam) tl = T_lam[slot];
-        o = slot < (unsigned long long)kLRThreads * kSeg ? (int)(slot / kSeg) : (int)T_own[slot];
+        o = slot < kSegSlots ? (int)(slot / kSeg) : (int)T_own[slot];
       }
       __syncthreads();                                                     // (C)
       // s_dead is a sticky flag (0 -> nonzero, never back): written and read
       // with shared-memory atomics; a stale 0 only costs one pruned-late node
       if (have && atomicAdd(&s_dead[o], 0) == 0) {
-        const uint32_t n_owner = (uint32_t)(p.shard_base + (unsigned long long)batch * kLRThreads + o);
+        const uint32_t n_owner = (uint32_t)(p.shard_base + bbase + o);
         drw += 2;
         NodeOut out;
         const int res = M::node(ts, tl, tidv, s_own[o], n_owner, epoch, seed, rho, out);
@@ -412,30 +460,39 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
         }
       }
       __syncthreads();                                                     // (D)
-      if (s_cnt[tid] > kSeg) s_cnt[tid] = kSeg;
+#pragma unroll
+      for (int q = 0; q < kOPT; ++q)
+        if (s_cnt[kOPT * tid + q] > kSeg) s_cnt[kOPT * tid + q] = kSeg;
       ++rounds;
     }
     max_rounds = rounds > max_rounds ? rounds : max_rounds;
-    max_nodes = s_nodes[tid] > max_nodes ? s_nodes[tid] : max_nodes;
-    // ---------------- phase 3: finish the particle
-    if (valid) {
-      if (active) {
-        const int dead = s_dead[tid];
-        if (dead) {
-          lw = -INFINITY;
-          if (dead == 2) ++ovf;
-        } else {
-          for (int k = 0; k < K; ++k) lw = lw + kLn2;
+    // ---------------- phase 3: finish the particles (phase-1 mapping)
+#pragma unroll
+    for (int q = 0; q < kOPT; ++q) {
+      const int o = q * kLRThreads + tid;
+      const unsigned long long i = bbase + o;
+      max_nodes = s_nodes[o] > max_nodes ? s_nodes[o] : max_nodes;
+      if (i < p.n_local) {
+        double w = lw[q];
+        if (act[q]) {
+          const int dead = s_dead[o];
+          if (dead) {
+            w = -INFINITY;
+            if (dead == 2) {
+              ++ovf;
+              atomicMin(&p.ctrl->first_err, (unsigned long long)(p.shard_base + i));
+            }
+          } else {
+            for (int k = 0; k < K[q]; ++k) w = w + kLn2;
+          }
         }
-        M::store(st, p.planes, p.n_local, i);
-        if (dead == 2) atomicMin(&p.ctrl->first_err, (unsigned long long)n_glob);
+        p.lw[i] = w;
+        if (alive_end[q]) ++n_end;
+        const bool b = isnan(w) || w == INFINITY;
+        bad |= b;
+        const long long kk = order_key(w);
+        key = kk > key ? kk : key;
       }
-      p.lw[i] = lw;
-      if (M::pc(st) != kStop) ++n_end;
-      const bool b = isnan(lw) || lw == INFINITY;
-      bad |= b;
-      const long long k = order_key(lw);
-      key = k > key ? k : key;
     }
     __syncthreads();
   }

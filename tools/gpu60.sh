@@ -1,0 +1,3 @@
+timeout 1800 python -m pytest tests -m gpu -q -x -k "lineage or LR or graph or shards or two_processes or inplace_full or statistics" 2>&1 | tail -2
+for w in crbd clads2; do timeout 400 python bench.py --workload $w --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['config']['workload'], round(d['ms_per_step'],2), '%.4g'%d['value'], d.get('phase_ms'))"; done
+python tools/diag_epochs.py crbd 2>&1 | grep -v Exception
