@@ -251,7 +251,9 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
   __shared__ int s_cnt[kOwners];             // tasks in owner o's segment
   __shared__ int s_sel[kLRThreads];          // this round: lane -> task slot (owner-written)
   __shared__ int s_ovtop;                     // overflow stack top
-  __shared__ int s_wsum[kLRThreads / 32];
+  // 16-byte aligned: its vectorised read after barrier (A) must not cover the
+  // neighbouring s_ovtop, which thread 0 writes after (A) (racecheck)
+  __shared__ __align__(16) int s_wsum[kLRThreads / 32];
   __shared__ unsigned s_batch;
   __shared__ int s_dead[kOwners];             // 0 alive, 1 detected/rejected, 2 node cap
   __shared__ unsigned s_nodes[kOwners];
@@ -370,6 +372,7 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
         if (c > kSeg) s_cnt[o] = kSeg;          // pushes beyond the segment went to overflow
         c0 += c > 0;
       }
+      __syncwarp();   // bar.red needs a converged warp (synccheck)
       n_act = __syncthreads_count(c0 > 0) * kOPT;   // estimate for the first round's share
     }
     unsigned rounds = 0;
@@ -393,6 +396,7 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
       }
       if (lane_id == 31) s_wsum[warp_id] = incl;
       const int ov = min(*(volatile int*)&s_ovtop, kOverflowCap);
+      __syncwarp();
       __syncthreads();                                                     // (A)
       int woff = 0, tot = 0;
 #pragma unroll

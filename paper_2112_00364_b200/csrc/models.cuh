@@ -200,20 +200,24 @@ struct Clads2 {
   __device__ static bool bad_rate(double r) { return !(r <= kMaxRate); }
 
   struct State { double sigma, alpha, eps, lam; double pend[kPend]; int pc, branch, sp; };
+  // The pending-rate stack is pend[0, sp): planes beyond the stack pointer are
+  // neither read nor written (the copies skip them too).
   __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
-    uint4 v = ldp(P, st, 0, i); s.sigma = lo_d(v); s.alpha = hi_d(v);
+    uint4 v = ldp(P, st, 5, i); s.pc = (int)v.x; s.branch = (int)v.y; s.sp = (int)v.z;
+    v = ldp(P, st, 0, i); s.sigma = lo_d(v); s.alpha = hi_d(v);
     v = ldp(P, st, 1, i); s.eps = lo_d(v); s.lam = hi_d(v);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      v = ldp(P, st, 2 + k, i); s.pend[2 * k] = lo_d(v); s.pend[2 * k + 1] = hi_d(v);
+      v = 2 * k < s.sp ? ldp(P, st, 2 + k, i) : make_uint4(0u, 0u, 0u, 0u);
+      s.pend[2 * k] = lo_d(v); s.pend[2 * k + 1] = hi_d(v);
     }
-    v = ldp(P, st, 5, i); s.pc = (int)v.x; s.branch = (int)v.y; s.sp = (int)v.z;
   }
   __device__ static void store(const State& s, uint4* P, unsigned long long st, unsigned long long i) {
     stp(P, st, 0, i, pack_dd(s.sigma, s.alpha));
     stp(P, st, 1, i, pack_dd(s.eps, s.lam));
 #pragma unroll
-    for (int k = 0; k < 3; ++k) stp(P, st, 2 + k, i, pack_dd(s.pend[2 * k], s.pend[2 * k + 1]));
+    for (int k = 0; k < 3; ++k)
+      if (2 * k < s.sp) stp(P, st, 2 + k, i, pack_dd(s.pend[2 * k], s.pend[2 * k + 1]));
     stp(P, st, 5, i, make_uint4((uint32_t)s.pc, (uint32_t)s.branch, (uint32_t)s.sp, 0u));
   }
   __device__ static int pc(const State& s) { return s.pc; }
