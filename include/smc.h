@@ -206,6 +206,16 @@ int smc_set_ess_threshold(smc_handle h, uint32_t a, uint32_t b);
  * per-phase timing, which force the host loop automatically). */
 int smc_set_graph(smc_handle h, int32_t on);
 
+/* Resampling launch shape.  *grid_out = the CTA count of the
+ * single cooperative launch that performs a whole resampling step (rows
+ * a6-a10: quantise + exact u128 sum, grid barrier, ancestors + gather,
+ * log Z), chosen at create time when the handle holds one shard, resamples
+ * out of place and its particles fit the co-resident grid's shared memory
+ * (12 B each); 0 = the split reduce / anc_gather / finalize kernels (several
+ * shards, in-place, large N, or env SMC_NO_FUSED_RESAMPLE=1 at create).
+ * Both paths give bit-identical results.  Returns SMC_EINVAL on NULL. */
+int smc_resample_grid(smc_handle h, int32_t* grid_out);
+
 /* Per-phase CUDA-event timing of every epoch (off by default).  The times
  * accumulate into smc_stats_t.ms_propagate / ms_resample until smc_reset. */
 int smc_set_timing(smc_handle h, int32_t on);

@@ -101,6 +101,7 @@ _sig = {
     "smc_resample_host": ([H, C.POINTER(C.c_double), C.c_void_p, C.c_void_p,
                            C.POINTER(C.c_uint32), C.c_uint32, C.POINTER(C.c_double)], C.c_int),
     "smc_last_distinct": ([H, C.POINTER(C.c_uint64)], C.c_int),
+    "smc_resample_grid": ([H, C.POINTER(C.c_int32)], C.c_int),
     "smc_load": ([H, C.c_void_p, C.c_void_p, C.c_int32], C.c_int),
     "smc_resample_step": ([H, C.c_uint32], C.c_int),
     "smc_plan_ranges": ([C.POINTER(C.c_uint64), C.c_int32, C.c_uint64, C.c_uint64,
@@ -242,6 +243,12 @@ class Smc:
 
     def set_graph(self, on=True):
         _check(self.h, _lib.smc_set_graph(self.h, 1 if on else 0))
+
+    def resample_grid(self):
+        """CTAs of the single-launch fused resampling step (0: split kernels)."""
+        v = C.c_int32(0)
+        _check(self.h, _lib.smc_resample_grid(self.h, C.byref(v)))
+        return v.value
 
     def set_timing(self, on=True):
         _check(self.h, _lib.smc_set_timing(self.h, 1 if on else 0))

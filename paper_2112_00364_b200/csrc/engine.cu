@@ -87,6 +87,11 @@ struct smc_ctx {
   bool lineage = false;           // §R-18 lineage-keyed side trees (SMC_FLAG_LINEAGE_RNG)
   bool analytic = false;          // §R-20 CRBD with 2E(t) per hidden event (SMC_FLAG_ANALYTIC_UNDETECTED)
   bool inplace = false;           // §R-21 permuted ancestors, one state buffer (SMC_FLAG_INPLACE)
+  int fused_grid = 0;             // > 0: single-shard resampling in one cooperative launch
+  int fused_ipt = 0;              // particles per thread of resample_fused_kernel
+  size_t fused_smem = 0;
+  u128* d_blk_sum = nullptr;      // [fused_grid]
+  U192* d_blk_q2 = nullptr;       // [fused_grid]
   bool stack_prefix = true;       // §R-22 copy only the used stack prefix (env SMC_NO_STACK_PREFIX=1: off, diagnostics)
   int lr_grid = 0;                // persistent grid of the cooperative kernel
   int prop_grid = 0;              // resident-CTA grid of propagate_kernel<M> (grid-stride)
@@ -391,6 +396,56 @@ int reset_device(smc_ctx* h) {
   return SMC_OK;
 }
 
+// Fused single-launch resampling (resample_fused_kernel): one shard in this
+// process, out of place, and the shard's particles fit the co-resident grid's
+// shared memory at 12 B each (q and O_k).  Env SMC_NO_FUSED_RESAMPLE=1 keeps
+// the split reduce / anc_gather / finalize path (A/B measurements).
+const void* fused_fn(int planes) {
+  switch (planes) {
+    case 1: return (const void*)resample_fused_kernel<1>;
+    case 2: return (const void*)resample_fused_kernel<2>;
+    case 4: return (const void*)resample_fused_kernel<4>;
+    case 6: return (const void*)resample_fused_kernel<6>;
+    case 8: return (const void*)resample_fused_kernel<8>;
+    default: return (const void*)resample_fused_kernel<0>;
+  }
+}
+int plan_fused(smc_ctx* h) {
+  h->fused_grid = 0;
+  const char* off = std::getenv("SMC_NO_FUSED_RESAMPLE");
+  if ((off && off[0] == '1') || h->world != 1 || h->n_local_shards != 1 || h->inplace ||
+      h->kind == SMC_RESAMPLE_BENCH)
+    return SMC_OK;
+  int dev = 0, sms = 0, optin = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  int coop = 0;
+  CU(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+  if (!coop) return SMC_OK;
+  const void* fn = fused_fn(h->planes);
+  const unsigned long long n = h->n_per;
+  for (int per_sm : {2, 1}) {
+    const unsigned long long g0 = (unsigned long long)sms * per_sm;
+    const unsigned long long ipt = std::max(1ull, (n + g0 * kFT - 1) / (g0 * kFT));
+    const size_t smem = (size_t)ipt * kFT * 12 + 4;      // q and O_k per particle
+    if (smem + 8192 > (size_t)optin) continue;
+    CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int nb = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kFT, smem));
+    if (nb < per_sm) continue;
+    const unsigned long long grid = (n + ipt * kFT - 1) / (ipt * kFT);
+    if (grid > (unsigned long long)kMaxFusedGrid) continue;
+    h->fused_grid = (int)grid;
+    h->fused_ipt = (int)ipt;
+    h->fused_smem = smem;
+    CU(cudaMalloc(&h->d_blk_sum, grid * sizeof(u128)));
+    CU(cudaMalloc(&h->d_blk_q2, grid * sizeof(U192)));
+    return SMC_OK;
+  }
+  return SMC_OK;
+}
+
 int common_init(smc_ctx* h, const smc_model* m, unsigned long long n_per, int world, int rank,
                 int n_local_shards, unsigned long long seed) {
   int rc = setup_model(h, m);
@@ -456,6 +511,8 @@ int common_init(smc_ctx* h, const smc_model* m, unsigned long long n_per, int wo
   }
   if (h->inplace && world > 1)
     return fail(h, SMC_EINVAL, "SMC_FLAG_INPLACE needs a single shard (no cross-shard hole matching yet)");
+  rc = plan_fused(h);
+  if (rc) return rc;
   h->shards.resize(n_local_shards);
   for (int i = 0; i < n_local_shards; ++i) {
     Shard& s = h->shards[i];
@@ -642,7 +699,7 @@ void launch_reduce(smc_ctx* h, const ResArgs& a) {
   if (h->items == kItemsSmall) reduce_kernel<kItemsSmall><<<grid, kThreads, 0, h->stream>>>(a);
   else reduce_kernel<kItems><<<grid, kThreads, 0, h->stream>>>(a);
 }
-void launch_finalize(smc_ctx* h, Shard& s) {
+FinArgs fin_args(smc_ctx* h, Shard& s) {
   FinArgs f;
   f.recA = h->d_recA;
   f.recB = h->d_recB;
@@ -651,7 +708,30 @@ void launch_finalize(smc_ctx* h, Shard& s) {
   f.n_total = h->n_total;
   f.strict = (h->flags & SMC_FLAG_STRICT) ? 1 : 0;
   f.ctrl = s.ctrl;
-  finalize_kernel<<<1, 32, 0, h->stream>>>(f);
+  return f;
+}
+int launch_fused(smc_ctx* h, Shard& s, const ResArgs& a) {
+  FusedArgs f;
+  f.blk_sum = h->d_blk_sum;
+  f.blk_q2 = h->d_blk_q2;
+  f.ipt = h->fused_ipt;
+  f.fin = fin_args(h, s);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)h->fused_grid);
+  cfg.blockDim = dim3(kFT);
+  cfg.dynamicSmemBytes = h->fused_smem;
+  cfg.stream = h->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;        // co-residency for the grid barrier
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  void* args[] = {(void*)&a, (void*)&f};
+  CU(cudaLaunchKernelExC(&cfg, fused_fn(h->planes), args));
+  return SMC_OK;
+}
+void launch_finalize(smc_ctx* h, Shard& s) {
+  finalize_kernel<<<1, 32, 0, h->stream>>>(fin_args(h, s));
 }
 
 // One epoch for all local shards (no host synchronisation unless the comm
@@ -666,6 +746,15 @@ int enqueue_epoch(smc_ctx* h) {
   if (h->timing) CU(cudaEventRecord(h->ev[1], h->stream));
   int rc = allgather_rec(h, h->d_recA + cur * h->world, rec);
   if (rc) return rc;
+  if (h->fused_grid > 0) {               // single shard: one launch for the whole resampling step
+    Shard& s = h->shards[0];
+    rc = launch_fused(h, s, res_args(h, s, s.lw, s.planes[cur], cur ^ 1));
+    if (rc) return rc;
+    CU(cudaGetLastError());
+    if (h->timing) CU(cudaEventRecord(h->ev[2], h->stream));
+    h->enq++;
+    return SMC_OK;
+  }
   for (auto& s : h->shards) {
     launch_reduce(h, res_args(h, s, s.lw, s.planes[cur], cur ^ 1));
   }
@@ -914,6 +1003,7 @@ void smc_destroy(smc_handle h) {
     cudaFree(s.scratch);
   }
   cudaFree(h->d_table); cudaFree(h->d_logfact); cudaFree(h->d_recA); cudaFree(h->d_recB); cudaFree(h->d_barrier);
+  cudaFree(h->d_blk_sum); cudaFree(h->d_blk_q2);
   cudaFree(h->tasks.sid); cudaFree(h->tasks.lam); cudaFree(h->tasks.owner);
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
   if (h->graph) cudaGraphDestroy(h->graph);
@@ -1308,6 +1398,12 @@ int smc_resample_step(smc_handle h, uint32_t epoch) {
   CU(cudaGetLastError());
   h->enq++;
   h->started = true;
+  return SMC_OK;
+}
+
+int smc_resample_grid(smc_handle h, int32_t* grid_out) {
+  if (!h || !grid_out) return fail(h, SMC_EINVAL, "NULL argument");
+  *grid_out = h->fused_grid;
   return SMC_OK;
 }
 

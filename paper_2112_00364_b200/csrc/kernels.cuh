@@ -66,6 +66,7 @@ struct Ctrl {
   unsigned long long side_roots;     // diag: hidden events (side-tree roots) generated
   unsigned max_side_nodes;           // diag: largest per-particle side-tree node count
   unsigned holes;                    // in-place resampling (R-21): slots without offspring
+  unsigned bar_count, bar_gen;       // grid barrier of resample_fused_kernel
 };
 
 enum { ST_OK = 0, ST_REJECTED = 4, ST_NAN = 5, ST_OVERFLOW = 6 };
@@ -75,6 +76,12 @@ __device__ __forceinline__ u128 shfl_up_u128(u128 v, int d) {
   unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
   lo = __shfl_up_sync(0xffffffffu, lo, d);
   hi = __shfl_up_sync(0xffffffffu, hi, d);
+  return ((u128)hi << 64) | lo;
+}
+__device__ __forceinline__ u128 shfl_idx_u128(u128 v, int src) {
+  unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
+  lo = __shfl_sync(0xffffffffu, lo, src);
+  hi = __shfl_sync(0xffffffffu, hi, src);
   return ((u128)hi << 64) | lo;
 }
 __device__ __forceinline__ u128 shfl_xor_u128(u128 v, int d) {
@@ -190,14 +197,17 @@ struct Grid {
   unsigned long long z2p1;   // 2z + 1
   unsigned long long N;
   double Wd, Nd, ud;
+  double NdWd;               // N / W (fp64)
   // P(j, C): grid point j lies strictly below cumulative weight C.
   __device__ __forceinline__ bool below(unsigned long long j, u128 C) const {
     const u128 A = ((u128)j << 54) + z2p1;
     return lt_u256(mul_u128(A, W), mul_u128(Nsc, C));
   }
   // F(C) = #{j in [0, N) : (j + u) W < N C} = clamp(ceil(N C / W - u), 0, N).
+  // The fp64 estimate (relative error a few ulps, i.e. < 2^-19 absolute for
+  // N < 2^32) only selects the exact 192-bit fix-up near integers.
   __device__ __forceinline__ unsigned long long count_below(u128 C) const {
-    const double x = Nd * (u128_approx(C) / Wd) - ud;
+    const double x = u128_approx(C) * NdWd - ud;
     const double r = rint(x);
     if (fabs(x - r) > 0x1p-12) {
       double c = ceil(x);
@@ -597,6 +607,19 @@ __device__ __forceinline__ Grid make_grid(const ResArgs& a, const RecB* B, unsig
   gr.Wd = u128_approx(W);
   gr.Nd = (double)a.n_total;
   gr.ud = (double)gr.z2p1 * 0x1p-54;
+  gr.NdWd = gr.Nd / gr.Wd;
+  return gr;
+}
+__device__ __forceinline__ Grid make_grid_w(u128 W, unsigned long long n_total, unsigned long long z) {
+  Grid gr;
+  gr.W = W;
+  gr.N = n_total;
+  gr.Nsc = (u128)n_total << 54;
+  gr.z2p1 = 2ull * z + 1ull;
+  gr.Wd = u128_approx(W);
+  gr.Nd = (double)n_total;
+  gr.ud = (double)gr.z2p1 * 0x1p-54;
+  gr.NdWd = gr.Nd / gr.Wd;
   return gr;
 }
 
@@ -946,8 +969,7 @@ struct FinArgs {
   int strict;
   Ctrl* ctrl;
 };
-__global__ void finalize_kernel(FinArgs a) {
-  if (threadIdx.x != 0) return;
+__device__ __noinline__ void finalize_body(const FinArgs& a) {
   Ctrl* c = a.ctrl;
   if (c->done) return;
   const unsigned epoch = c->epoch;
@@ -996,6 +1018,9 @@ __global__ void finalize_kernel(FinArgs a) {
   RecB* nb = a.recB + (par ^ 1) * a.world + a.rank;
   nb->W = 0;
   nb->q2[0] = nb->q2[1] = nb->q2[2] = 0;
+}
+__global__ void finalize_kernel(FinArgs a) {
+  if (threadIdx.x == 0) finalize_body(a);
 }
 
 // ============================================================================
@@ -1080,6 +1105,302 @@ __global__ void __launch_bounds__(kThreads) max_kernel(const double* lw, unsigne
     atomicMax(&r->key, k);
     if (s_bad) atomicOr(&r->flags, 1u);
   }
+}
+
+
+// ============================================================================
+// resample_fused: the whole resampling step of a single-shard run in ONE
+// cooperative launch (rows a6-a10 + finalize), for shards whose particles fit
+// the grid's shared memory (12 B each: 10^6 particles = 12 MB over 148 SMs).  Phase 1: each CTA
+// loads its contiguous block of log-weights once, quantises them in shared
+// memory (the same q = quantize(lw, m) as reduce) and publishes its u128 block
+// sum (and sum q^2 for the ESS gate); grid barrier; phase 2: every CTA derives
+// the identical exact total W and its block's exclusive prefix from the block
+// sums, CTA 0 folds the epoch into log Z (finalize_body), and each CTA maps its
+// particles to offspring boundaries O_k = F(C_k) and gathers the output slots
+// they own — the second weight pass reads shared memory, not HBM, and one
+// launch replaces reduce + anc_gather + finalize.  Results are identical to
+// the split path (same integers, same grid, same slot ownership).
+// ============================================================================
+constexpr int kFT = 512;                 // threads per fused CTA
+#ifndef SMC_FUSED_MINB
+#define SMC_FUSED_MINB 2                 // resident CTAs per SM (register cap 64)
+#endif
+constexpr int kMaxFusedGrid = 1024;
+
+struct FusedArgs {
+  u128* blk_sum;                         // [grid]
+  U192* blk_q2;                          // [grid]
+  int ipt;                               // particles per thread (block = kFT * ipt)
+  FinArgs fin;
+};
+
+__device__ __forceinline__ void grid_barrier(Ctrl* c) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = &c->bar_gen;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(&c->bar_count, 1u) == gridDim.x - 1) {
+      c->bar_count = 0;
+      __threadfence();
+      atomicExch(&c->bar_gen, g + 1u);
+    } else {
+      while (*gen == g) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// One output slot: copy particle `src`'s planes (stack prefix only, R-22).
+template <int P>
+__device__ __forceinline__ void copy_particle(const ResArgs& a, uint4* dst, unsigned long long src,
+                                              unsigned long long slot, int skip) {
+  if (P > 0) {
+    uint4 v[P > 0 ? P : 1];
+#pragma unroll
+    for (int p = 0; p < (P > 0 ? P : 1); ++p)
+      if (copy_plane(a, p, skip)) v[p] = __ldg(a.src_planes + (unsigned long long)p * a.n_local + src);
+#pragma unroll
+    for (int p = 0; p < (P > 0 ? P : 1); ++p)
+      if (copy_plane(a, p, skip)) dst[(unsigned long long)p * a.n_local + slot] = v[p];
+  } else {
+    for (int p = 0; p < a.planes; ++p)
+      if (copy_plane(a, p, skip))
+        dst[(unsigned long long)p * a.n_local + slot] = __ldg(a.src_planes + (unsigned long long)p * a.n_local + src);
+  }
+}
+
+// Layout: CTA b owns particles [b*kFT*ipt, (b+1)*kFT*ipt); round r of a CTA
+// covers its particles r*kFT + t (t = thread), so every round is a contiguous
+// run of kFT particles, scanned across the CTA, and a thread writes the
+// offspring slots [O_{k-1}, O_k) of its own particle k (consecutive threads,
+// consecutive slots: coalesced; no search).
+template <int P>   // planes per particle (<= 0: runtime a.planes)
+__global__ void __launch_bounds__(kFT, SMC_FUSED_MINB) resample_fused_kernel(ResArgs a, FusedArgs f) {
+  extern __shared__ unsigned long long s_q[];          // [kFT * ipt] quantised weights
+  __shared__ u128 s_w[2][kFT / 32];
+  __shared__ u128 s_w2[kFT / 32];
+  __shared__ U192 s_q2[kFT / 32];
+  Ctrl* c = a.ctrl;
+  const int ipt = f.ipt;
+  const int blk = kFT * ipt;
+  const unsigned long long base = (unsigned long long)blockIdx.x * blk;
+  const int cnt = base < a.n_local ? (int)min((unsigned long long)blk, a.n_local - base) : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // ---- phase 1: striped (coalesced) load into shared memory, issued before
+  // the control reads it does not depend on; each thread then quantises its
+  // blocked items k = t*ipt + r in place and sums them; one CTA scan gives
+  // every thread the exclusive prefix of its items and the block sum
+  for (int r0 = 0; r0 < ipt; r0 += 4) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = (r0 + u) * kFT + threadIdx.x;
+      v[u] = (r0 + u < ipt && k < cnt) ? __ldg(a.lw + base + k) : -INFINITY;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (r0 + u < ipt) s_q[(r0 + u) * kFT + threadIdx.x] = (unsigned long long)__double_as_longlong(v[u]);
+  }
+  if (*(volatile unsigned*)&c->done) return;          // read by every CTA before the barrier
+  const unsigned epoch = c->epoch;
+  const unsigned par = epoch & 1;
+  const bool ess = c->ess_a < c->ess_b;
+  const Global G = read_global(a.recA + par * a.world, a.world);
+  // the last CTA (fewest particles: the ragged tail) folds the epoch into log Z
+  const bool fin_cta = blockIdx.x == gridDim.x - 1;
+  if (!G.ok) {                                          // error / all rejected: finalize only
+    if (fin_cta && threadIdx.x == 0) finalize_body(f.fin);
+    return;
+  }
+  __syncthreads();
+  u128 tsum = 0, tq2 = 0;
+  for (int r = 0; r < ipt; ++r) {
+    const int k = threadIdx.x * ipt + r;
+    const unsigned long long q = quantize(__longlong_as_double((long long)s_q[k]), G.m);
+    s_q[k] = q;
+    tsum += q;
+    if (ess) tq2 += (u128)q * q;
+  }
+  u128 incl = tsum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const u128 o = shfl_up_u128(incl, d);
+    if (lane >= d) incl += o;
+  }
+  if (lane == 31) s_w[0][warp] = incl;
+  if (ess) {
+    U192 q2;
+    q2.w[0] = (unsigned long long)tq2; q2.w[1] = (unsigned long long)(tq2 >> 64); q2.w[2] = 0;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) add_u192(q2, shfl_xor_u192(q2, d));
+    if (lane == 0) s_q2[warp] = q2;
+  }
+  __syncthreads();
+  // warp totals -> their inclusive scan across the 16 warps, in every warp's
+  // lanes 0..15 (4 shuffle steps instead of 16 shared loads per thread)
+  u128 ws = lane < kFT / 32 ? s_w[0][lane] : (u128)0;
+#pragma unroll
+  for (int d = 1; d < kFT / 32; d <<= 1) {
+    const u128 o = shfl_up_u128(ws, d);
+    if (lane >= d) ws += o;
+  }
+  const u128 woff = warp ? shfl_idx_u128(ws, warp - 1) : (u128)0;
+  const u128 bsum = shfl_idx_u128(ws, kFT / 32 - 1);
+  const u128 texcl = woff + incl - tsum;                // exclusive prefix of this thread's items
+  if (threadIdx.x == 0) {
+    f.blk_sum[blockIdx.x] = bsum;
+    if (ess) {
+      U192 q = s_q2[0];
+      for (int w = 1; w < kFT / 32; ++w) add_u192(q, s_q2[w]);
+      f.blk_q2[blockIdx.x] = q;
+    }
+  }
+  grid_barrier(c);
+  // ---- phase 2: exact totals (identical in every CTA), finalize, ancestors + gather
+  u128 tot = 0, pre = 0;
+  U192 q2t = {{0, 0, 0}};
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += kFT) {
+    const u128 v = ld_cg_u128(f.blk_sum + b);
+    tot += v;
+    if (b < (int)blockIdx.x) pre += v;
+    if (ess) {
+      const unsigned long long* src = (const unsigned long long*)(f.blk_q2 + b);
+      U192 t;
+      t.w[0] = __ldcg(src); t.w[1] = __ldcg(src + 1); t.w[2] = __ldcg(src + 2);
+      add_u192(q2t, t);
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    tot += shfl_xor_u128(tot, d);
+    pre += shfl_xor_u128(pre, d);
+    if (ess) add_u192(q2t, shfl_xor_u192(q2t, d));
+  }
+  if (lane == 0) { s_w[1][warp] = tot; s_w2[warp] = pre; if (ess) s_q2[warp] = q2t; }
+  __syncthreads();
+  tot = lane < kFT / 32 ? s_w[1][lane] : (u128)0;
+  pre = lane < kFT / 32 ? s_w2[lane] : (u128)0;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    tot += shfl_xor_u128(tot, d);
+    pre += shfl_xor_u128(pre, d);
+  }
+  if (ess) {
+    q2t = {{0, 0, 0}};
+    for (int w = 0; w < kFT / 32; ++w) add_u192(q2t, s_q2[w]);
+  }
+  if (fin_cta && threadIdx.x == 0) {
+    RecB* rb = a.recB + par * a.world + a.rank;
+    rb->W = tot;
+    rb->q2[0] = q2t.w[0]; rb->q2[1] = q2t.w[1]; rb->q2[2] = q2t.w[2];
+    finalize_body(f.fin);                               // log Z, termination, epoch advance
+  }
+  if (G.alive == 0) return;                             // final epoch: no resample
+  uint4* dst = a.dst_planes[a.rank];
+  if (!ess_resample(tot, q2t, a.n_total, c->ess_a, c->ess_b)) {
+    for (int k = threadIdx.x; k < cnt; k += kFT)        // ESS high: identity copy (R-19)
+      copy_particle<P>(a, dst, base + k, base + k, stack_skip_lo(a, a.src_planes, base + k));
+    return;
+  }
+  const unsigned long long seed = c->seed;
+  const uint4 rr = philox4x32_10(make_uint4(0u, epoch, 0u, 1u), (uint32_t)seed, (uint32_t)(seed >> 32));
+  const Grid gr = make_grid_w(tot, a.n_total, hq_bits(rr.x, rr.y));
+  uint32_t* anc = a.dst_anc[a.rank];
+  unsigned* s_O = reinterpret_cast<unsigned*>(s_q + blk);   // [blk] offspring boundaries O_k
+  // 2a: O_k = F(C_k) for the thread's blocked items (shared memory only)
+  u128 C = pre + texcl;
+  unsigned distinct = 0;                                // particles with offspring
+  unsigned prevO = (unsigned)gr.count_below(C);
+  for (int r = 0; r < ipt; ++r) {
+    const int k = threadIdx.x * ipt + r;
+    C += s_q[k];
+    const unsigned O = (unsigned)gr.count_below(C);     // zero weight: O_k = O_{k-1}
+    s_O[k] = O;
+    distinct += O > prevO;
+    prevO = O;
+  }
+  if (threadIdx.x == 0) s_O[blk] = (unsigned)gr.count_below(pre);   // O before the block
+  __syncthreads();
+  // 2b: output slots.  Warp w's particles [w*32*ipt, (w+1)*32*ipt) (the
+  // blocked items of its lanes) fill the contiguous slots [O_{first-1},
+  // O_last); the lanes take consecutive slots and find their source by a
+  // binary search over the warp's O values (coalesced stores, no barriers).
+  // If one warp owns more than kHeavy slots per particle on average (a few
+  // dominant weights), the whole CTA instead shares the block's slots, so a
+  // single heavy particle is copied by kFT threads, not 32.
+  constexpr unsigned kHeavy = 8;
+  __shared__ unsigned s_heavy;
+  if (threadIdx.x == 0) s_heavy = 0;
+  __syncthreads();
+  const int wk0 = warp * 32 * ipt, wn = 32 * ipt;       // the warp's particles
+  const unsigned wA = wk0 ? s_O[wk0 - 1] : s_O[blk];
+  const unsigned wB = s_O[wk0 + wn - 1];
+  if (lane == 0 && wB - wA > kHeavy * (unsigned)wn) atomicOr(&s_heavy, 1u);
+  __syncthreads();
+  if (!s_heavy) {
+    // U chunks of 32 slots per iteration: U independent searches, then all
+    // loads, then all stores (U*P 16-byte loads in flight per lane)
+    constexpr int U = P == 1 ? 4 : P == 2 ? 2 : 1;
+    for (unsigned j0 = wA + lane; j0 < wB; j0 += 32 * U) {
+      int src[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned j = j0 + 32 * u;
+        int lo = wk0, hi = wk0 + wn - 1;                // first particle with O_k > j
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (s_O[mid] > j) hi = mid; else lo = mid + 1;
+        }
+        src[u] = lo;
+      }
+      if (P > 0 && P <= 2 && a.stk_n == 0) {            // whole-particle copies
+        uint4 v[U][P > 0 && P <= 2 ? P : 1];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int p = 0; p < (P > 0 && P <= 2 ? P : 1); ++p)
+            if (j0 + 32 * u < wB)
+              v[u][p] = __ldg(a.src_planes + (unsigned long long)p * a.n_local + base + src[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const unsigned j = j0 + 32 * u;
+          if (j < wB) {
+#pragma unroll
+            for (int p = 0; p < (P > 0 && P <= 2 ? P : 1); ++p) dst[(unsigned long long)p * a.n_local + j] = v[u][p];
+            anc[j] = (uint32_t)(a.shard_base + base + src[u]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const unsigned j = j0 + 32 * u;
+          if (j < wB) {
+            const unsigned long long sp = base + src[u];
+            copy_particle<P>(a, dst, sp, j, stack_skip_lo(a, a.src_planes, sp));
+            anc[j] = (uint32_t)(a.shard_base + sp);
+          }
+        }
+      }
+    }
+  } else {
+    const unsigned A = s_O[blk], B = s_O[blk - 1];
+    for (unsigned j = A + threadIdx.x; j < B; j += kFT) {
+      int lo = 0, hi = blk - 1;                         // first item with O_k > j
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s_O[mid] > j) hi = mid; else lo = mid + 1;
+      }
+      const unsigned long long src = base + lo;
+      copy_particle<P>(a, dst, src, j, stack_skip_lo(a, a.src_planes, src));
+      anc[j] = (uint32_t)(a.shard_base + src);
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) distinct += __shfl_xor_sync(0xffffffffu, distinct, d);
+  if (lane == 0 && distinct) atomicAdd(&c->distinct, (unsigned long long)distinct);
 }
 
 }  // namespace smc

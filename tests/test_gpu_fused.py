@@ -1,0 +1,166 @@
+"""The single-launch fused resampling step (resample_fused_kernel, DESIGN.md
+§7.6) against the split reduce / anc_gather / finalize kernels and the oracle.
+
+Both paths compute the same integers q = quantize(lw, m), the same exact total
+W, the same systematic grid and the same slot ownership, so every output —
+log-weights, ancestors, states, log Z, counters — must be bit-identical.  The
+split path is selected with SMC_NO_FUSED_RESAMPLE=1 at create time.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def make(smc, kind, data, params, N, seed, fused, flags=0, ess=None):
+    old = os.environ.pop("SMC_NO_FUSED_RESAMPLE", None)
+    if not fused:
+        os.environ["SMC_NO_FUSED_RESAMPLE"] = "1"
+    try:
+        if kind in (smc.CRBD, smc.CLADS2):
+            m = smc.Model(kind, smc.tree_data(data), params, flags=flags)
+        else:
+            m = smc.Model(kind, data, params, flags=flags)
+        h = smc.Smc(m, N, seed)
+    finally:
+        os.environ.pop("SMC_NO_FUSED_RESAMPLE", None)
+        if old is not None:
+            os.environ["SMC_NO_FUSED_RESAMPLE"] = old
+    if ess:
+        h.set_ess_threshold(*ess)
+    assert (h.resample_grid() > 0) == fused
+    return h
+
+
+def same(a, b):
+    np.testing.assert_array_equal(a.log_weights(), b.log_weights())
+    np.testing.assert_array_equal(a.ancestors(), b.ancestors())
+    np.testing.assert_array_equal(a.fields(), b.fields())
+
+
+CASES = [
+    ("crbd_lineage", "CRBD", "tree90", "CRBD_PARAMS", "FLAG_LINEAGE_RNG", None, 30_000),
+    ("crbd_seq", "CRBD", "tree5", "CRBD_PARAMS", None, None, 4099),
+    ("crbd_analytic_ess", "CRBD", "tree90", "CRBD_PARAMS", "FLAG_ANALYTIC_UNDETECTED", (1, 2), 50_000),
+    ("clads2_lineage", "CLADS2", "tree90", "CLADS2_PARAMS", "FLAG_LINEAGE_RNG", None, 20_000),
+    ("clads2_ess", "CLADS2", "tree5", "CLADS2_PARAMS", "FLAG_LINEAGE_RNG", (3, 4), 7777),
+    ("seir", "SEIR", None, None, None, None, 3000),
+    ("ssm", "SSM", None, "SSM_PARAMS", None, None, 100_003),
+    # peaked likelihood (obs. std 1e-4): a few particles take most offspring,
+    # which exercises the CTA-wide (heavy) slot assignment
+    ("ssm_peaked", "SSM", None, [0.0, 100.0, 2.0, 1.0, 1e-4], None, None, 200_000),
+    ("geometric_ess", "GEOMETRIC", None, None, None, (1, 2), 2049),
+    ("constw", "CONSTW", None, None, None, None, 1),
+]
+
+
+def case_args(smc, name, kind, data, params, flag, ess, N):
+    k = getattr(smc, kind)
+    if kind in ("CRBD", "CLADS2"):
+        d = inputs.tree(data)
+    elif kind == "SEIR":
+        d = inputs.seir_series()
+    elif kind == "SSM":
+        d = inputs.ssm_series(50)
+    else:
+        d = None
+    p = (getattr(inputs, params) if isinstance(params, str) else params) if params else None
+    if kind == "GEOMETRIC":
+        p = inputs.GEOMETRIC_PARAMS
+    elif kind == "CONSTW":
+        p = inputs.CONSTW_PARAMS
+    fl = getattr(smc, flag) if flag else 0
+    return k, d, p, fl, ess, N
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_fused_matches_split_per_epoch(smc, case):
+    k, d, p, fl, ess, N = case_args(smc, *case)
+    f = make(smc, k, d, p, N, 11, True, fl, ess)
+    s = make(smc, k, d, p, N, 11, False, fl, ess)
+    f.set_graph(False)
+    s.set_graph(False)
+    e = 0
+    while True:
+        rf, df = f.step()
+        rs, ds = s.step()
+        assert (rf, df) == (rs, ds)
+        if e < 12 or df:
+            same(f, s)
+        e += 1
+        if df:
+            break
+    assert f.log_z == s.log_z
+    sf, ss = f.stats(), s.stats()
+    # (draws are schedule-dependent under the lineage-keyed kernels: a side
+    # tree stops at its first detection, however many lanes were exploring it)
+    keys = ["epochs", "resamples", "alive_particle_steps", "overflow"]
+    if fl != getattr(smc, "FLAG_LINEAGE_RNG"):
+        keys.append("draws")
+    for key in keys:
+        assert sf[key] == ss[key], key
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_fused_graph_run_matches_split(smc, case):
+    k, d, p, fl, ess, N = case_args(smc, *case)
+    f = make(smc, k, d, p, N, 12, True, fl, ess)
+    s = make(smc, k, d, p, N, 12, False, fl, ess)
+    for seed in (12, 13):                 # a second sweep through the same graph
+        f.reset(seed)
+        s.reset(seed)
+        f.run()
+        s.run()
+        assert f.log_z == s.log_z
+        same(f, s)
+
+
+def test_fused_vs_oracle_crbd_tree90(smc):
+    """Per epoch against the oracle with the fused path active (several CTAs,
+    ragged last block)."""
+    N = 40_001
+    g = make(smc, smc.CRBD, inputs.tree("tree90"), inputs.CRBD_PARAMS, N, 21, True, smc.FLAG_LINEAGE_RNG)
+    g.set_graph(False)
+    o = oracle.Smc(oracle.CRBD_LR, oracle.tree_blob(inputs.tree("tree90")), inputs.CRBD_PARAMS, N, 21)
+    for _ in range(10):
+        rg, dg = g.step()
+        ro, do = o.step()
+        assert (rg, dg) == (ro, do)
+        lo, lg = o.lw(), g.log_weights()
+        f = np.isfinite(lo)
+        np.testing.assert_array_equal(np.isneginf(lg), np.isneginf(lo))
+        np.testing.assert_allclose(lg[f], lo[f], rtol=1e-9, atol=1e-12)
+        np.testing.assert_array_equal(g.ancestors(), o.anc())
+
+
+def test_fused_full_size_crbd(smc):
+    """BASELINE configs[1] size (10^6): whole graph run, fused vs split."""
+    N = 1_000_000
+    f = make(smc, smc.CRBD, inputs.tree("tree90"), inputs.CRBD_PARAMS, N, 3, True, smc.FLAG_LINEAGE_RNG)
+    s = make(smc, smc.CRBD, inputs.tree("tree90"), inputs.CRBD_PARAMS, N, 3, False, smc.FLAG_LINEAGE_RNG)
+    f.run()
+    s.run()
+    assert f.log_z == s.log_z
+    np.testing.assert_array_equal(f.ancestors(), s.ancestors())
+    np.testing.assert_array_equal(f.log_weights(), s.log_weights())
+    assert f.stats()["distinct"] == s.stats()["distinct"]
+
+
+def test_fused_rejected_and_large_n_fallback(smc):
+    # small N: every particle eventually has y_t > z_t -> EREJECTED on both paths
+    g = make(smc, smc.SEIR, inputs.seir_series(), None, 700, 31, True)
+    s = make(smc, smc.SEIR, inputs.seir_series(), None, 700, 31, False)
+    assert g.run_status() == s.run_status() == smc.EREJECTED
+    assert g.log_z == s.log_z
+    assert g.stats()["epochs"] == s.stats()["epochs"]
+    # a shard too large for the grid's shared memory takes the split path
+    big = smc.Smc(smc.Model(smc.CONSTW, None, inputs.CONSTW_PARAMS), 8_000_000, 1)
+    assert big.resample_grid() == 0
+    big.run()
+    # K = 4 checkpoints of weight 3 each: log Z = 4 ln 3 exactly up to rounding
+    assert big.log_z == pytest.approx(4 * np.log(3.0), rel=1e-14)
