@@ -103,6 +103,7 @@ struct smc_ctx {
   int world = 1, rank = 0;        // world = number of shards in the run
   int n_local_shards = 1;         // shards held by this handle
   int n_tiles = 0;
+  int chunk_tiles = 1, n_chunks = 0;   // reduce_kernel: one warp per chunk of tiles
   int items = kItems;             // particles per thread in a resampling tile
   unsigned long long seed = 0;
   ModelConst mc{};
@@ -466,6 +467,13 @@ int common_init(smc_ctx* h, const smc_model* m, unsigned long long n_per, int wo
   h->seed = seed;
   h->items = n_per <= kSmallN ? kItemsSmall : kItems;
   h->n_tiles = (int)((n_per + (unsigned long long)kThreads * h->items - 1) / ((unsigned long long)kThreads * h->items));
+  {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int target = sms * 3 * (kThreads / 32);      // 3 resident reduce CTAs per SM (85-register cap)
+    h->chunk_tiles = std::max(1, (h->n_tiles + target - 1) / target);
+    h->n_chunks = (h->n_tiles + h->chunk_tiles - 1) / h->chunk_tiles;
+  }
   CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   h->own_stream = true;
   if (!h->h_table.empty()) {
@@ -636,6 +644,8 @@ ResArgs res_args(smc_ctx* h, Shard& s, const double* lw, const uint4* src, int d
   a.tile_excl = s.tile_excl;
   a.tile_q2 = s.tile_q2;
   a.n_tiles = h->n_tiles;
+  a.chunk_tiles = h->chunk_tiles;
+  a.n_chunks = h->n_chunks;
   a.src_planes = src;
   a.planes = h->planes;
   a.dst_planes = s.d_dst_planes[dst_par];
@@ -695,7 +705,7 @@ void launch_resample_tail(smc_ctx* h, const ResArgs& a) {
   else launch_anc_gather(h, a);
 }
 void launch_reduce(smc_ctx* h, const ResArgs& a) {
-  const unsigned grid = (unsigned)((h->n_tiles + 1) / 2);     // two tiles per CTA
+  const unsigned grid = (unsigned)((h->n_chunks + kThreads / 32 - 1) / (kThreads / 32));   // a warp per chunk
   if (h->items == kItemsSmall) reduce_kernel<kItemsSmall><<<grid, kThreads, 0, h->stream>>>(a);
   else reduce_kernel<kItems><<<grid, kThreads, 0, h->stream>>>(a);
 }

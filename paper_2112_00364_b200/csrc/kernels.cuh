@@ -229,29 +229,42 @@ struct Grid {
 // polynomial (truncation 6e-18), scaled by 2^(k+62) in [2^-2, 2^62] — no
 // over/underflow paths.  Within ~2 ulp of exp(); both resampling passes use
 // this one function, so W and the prefixes are consistent.
+// Coefficients in constant memory: DFMA takes a constant-bank operand
+// directly, whereas 64-bit immediates cost two UMOVs per use (ncu: the reduce
+// pass was issue-bound with ~24 UMOVs per particle).
+__constant__ double kQuantC[16] = {
+    1.4426950408889634074,        // 1/ln 2
+    -6.93147180369123816490e-01,  // -ln 2 (high part)
+    -1.90821492927058770002e-10,  // -ln 2 (low part)
+    1.6059043836821614599e-10,    // 1/13!
+    2.0876756987868098979e-09,    // 1/12!
+    2.5052108385441718775e-08,
+    2.7557319223985890653e-07,
+    2.7557319223985890653e-06,
+    2.4801587301587301587e-05,
+    1.9841269841269841270e-04,
+    1.3888888888888888889e-03,
+    8.3333333333333333333e-03,
+    4.1666666666666666667e-02,
+    1.6666666666666666667e-01,
+    0.5,
+    -44.0};
 __device__ __forceinline__ unsigned long long quantize(double lw, double m) {
-  const double x = lw - m;
-  if (!(x >= -44.0)) return 0ull;                   // also lw = -inf
-  const double k = rint(x * 1.4426950408889634074);
-  double r = fma(k, -6.93147180369123816490e-01, x);
-  r = fma(k, -1.90821492927058770002e-10, r);
-  double p = 1.6059043836821614599e-10;             // 1/13!
-  p = fma(p, r, 2.0876756987868098979e-09);         // 1/12!
-  p = fma(p, r, 2.5052108385441718775e-08);
-  p = fma(p, r, 2.7557319223985890653e-07);
-  p = fma(p, r, 2.7557319223985890653e-06);
-  p = fma(p, r, 2.4801587301587301587e-05);
-  p = fma(p, r, 1.9841269841269841270e-04);
-  p = fma(p, r, 1.3888888888888888889e-03);
-  p = fma(p, r, 8.3333333333333333333e-03);
-  p = fma(p, r, 4.1666666666666666667e-02);
-  p = fma(p, r, 1.6666666666666666667e-01);
-  p = fma(p, r, 0.5);
+  const double x0 = lw - m;
+  const bool ok = x0 >= kQuantC[15];                // false for lw = -inf
+  const double x = ok ? x0 : 0.0;                   // branch-free: independent chains interleave
+  const double k = rint(x * kQuantC[0]);
+  double r = fma(k, kQuantC[1], x);
+  r = fma(k, kQuantC[2], r);
+  double p = kQuantC[3];
+#pragma unroll
+  for (int i = 4; i <= 14; ++i) p = fma(p, r, kQuantC[i]);
   p = fma(p, r, 1.0);
   p = fma(p, r, 1.0);
   const int e2 = (int)k + 62 + 1023;                // 2^(k+62), k in [-64, 0]
   const double scale = __hiloint2double(e2 << 20, 0);
-  return __double2ull_rn(p * scale);
+  const unsigned long long q = __double2ull_rn(p * scale);
+  return ok ? q : 0ull;
 }
 
 // ============================================================================
@@ -392,10 +405,12 @@ struct ResArgs {
   int world, rank;
   RecA* recA;                         // [2][world]
   RecB* recB;                         // [2][world] shard totals (W, sum q^2)
-  U192* tile_q2;                      // [n_tiles] (ESS only)
-  u128* tile_sum;                     // [n_tiles]
-  u128* tile_excl;                    // [n_tiles]
+  U192* tile_q2;                      // [n_chunks] chunk sums of q^2 (ESS only)
+  u128* tile_sum;                     // [n_chunks] chunk sums, then their exclusive prefix
+  u128* tile_excl;                    // [n_tiles] exclusive prefix of tile t within its chunk
   int n_tiles;
+  int chunk_tiles;                    // tiles per reduce chunk (one warp each)
+  int n_chunks;
   const uint4* src_planes;
   int planes;
   uint4* const* dst_planes;           // [world] destination buffers (peer pointers)
@@ -450,126 +465,135 @@ __device__ __forceinline__ Global read_global(const RecA* A, int world) {
 }
 
 // ============================================================================
-// reduce: per-tile u128 sums of q; the last CTA scans them
+// reduce: one warp per chunk of chunk_tiles consecutive tiles.  The warp walks
+// its tiles in order: 8 coalesced 16-byte loads per lane in flight, quantise,
+// warp-sum in u128, record the tile's exclusive prefix within the chunk and
+// advance the running chunk sum — no CTA barriers.  The last CTA (ticket)
+// scans the n_chunks chunk sums (exclusive prefix written back in place) and
+// publishes the shard total W (and sum q^2 for the ESS gate).  A tile's
+// exclusive prefix = tile_sum[t / chunk_tiles] + tile_excl[t].
 // ============================================================================
+__device__ __forceinline__ u128 tile_prefix(const ResArgs& a, int t) {
+  return ld_cg_u128(a.tile_sum + t / a.chunk_tiles) + ld_cg_u128(a.tile_excl + t);
+}
+
 template <int ITEMS>
-__global__ void __launch_bounds__(kThreads) reduce_kernel(ResArgs a) {
-  constexpr int kTile = kThreads * ITEMS;
-  constexpr int kItems = ITEMS;
-  constexpr int kTPB = 2;                               // tiles per CTA
-  __shared__ u128 s_w[kTPB][kThreads / 32];
-  __shared__ U192 s_q2[kTPB][kThreads / 32];
+__global__ void __launch_bounds__(kThreads, 3) reduce_kernel(ResArgs a) {
+  constexpr int kTile = kThreads * ITEMS;              // particles per tile
+  constexpr int kB = 4;                                // double2 loads per lane per batch (+ the next batch prefetched)
+  constexpr int kPerBatch = 32 * 2 * kB;               // 512 particles per warp batch
+  static_assert(kTile % kPerBatch == 0, "tile = whole batches");
+  __shared__ U192 s_q2[kThreads / 32];
   __shared__ unsigned s_ticket;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int chunk = blockIdx.x * (kThreads / 32) + warp;
+  const int t_lo = chunk * a.chunk_tiles;
+  const int t_hi = min(a.n_tiles, t_lo + a.chunk_tiles);
+  const double2* lw2 = reinterpret_cast<const double2*>(a.lw);
+  auto load_batch = [&](unsigned long long p0, double2 (&x)[kB]) {
+#pragma unroll
+    for (int b = 0; b < kB; ++b) {
+      const unsigned long long p = p0 + (unsigned long long)(b * 32 + lane) * 2;
+      if (p + 1 < a.n_local) x[b] = __ldg(lw2 + p / 2);
+      else {
+        x[b].x = p < a.n_local ? __ldg(a.lw + p) : -INFINITY;
+        x[b].y = -INFINITY;
+      }
+    }
+  };
+  double2 x[kB];
+  if (t_lo < t_hi) load_batch((unsigned long long)t_lo * kTile, x);   // before the control reads
   if (*(volatile unsigned*)&a.ctrl->done) return;
   const unsigned par = a.ctrl->epoch & 1;
-  const bool ess = a.ctrl->ess_a < a.ctrl->ess_b;         // uniform
+  const bool ess = a.ctrl->ess_a < a.ctrl->ess_b;      // uniform
   const Global G = read_global(a.recA + par * a.world, a.world);
   if (!G.ok) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double v[kTPB][kItems];
+  u128 run = 0;                                        // chunk sum (warp-uniform)
+  U192 q2 = {{0, 0, 0}};                               // lane's sum of q^2
+  for (int t = t_lo; t < t_hi; ++t) {
+    u128 ts = 0;
+    const unsigned long long p0 = (unsigned long long)t * kTile;
+    for (int bb = 0; bb < kTile / kPerBatch; ++bb) {
+      double2 y[kB];
 #pragma unroll
-  for (int tt = 0; tt < kTPB; ++tt) {                   // all loads first
-    const unsigned long long base = ((unsigned long long)blockIdx.x * kTPB + tt) * kTile;
-    if (base + kTile <= a.n_local) {
-      const double2* p = reinterpret_cast<const double2*>(a.lw + base);
+      for (int b = 0; b < kB; ++b) y[b] = x[b];
+      // prefetch the next batch (next tile's first at the end of this tile)
+      const bool last = bb == kTile / kPerBatch - 1;
+      if (!last) load_batch(p0 + (unsigned long long)(bb + 1) * kPerBatch, x);
+      else if (t + 1 < t_hi) load_batch(p0 + kTile, x);
 #pragma unroll
-      for (int r = 0; r < kItems / 2; ++r) {
-        const double2 t = __ldg(p + r * kThreads + threadIdx.x);
-        v[tt][2 * r] = t.x;
-        v[tt][2 * r + 1] = t.y;
-      }
-    } else {
-#pragma unroll
-      for (int r = 0; r < kItems; ++r) {
-        const unsigned long long i = base + (unsigned long long)r * kThreads + threadIdx.x;
-        v[tt][r] = i < a.n_local ? __ldg(a.lw + i) : -INFINITY;
+      for (int b = 0; b < kB; ++b) {
+        const unsigned long long q0 = quantize(y[b].x, G.m), q1 = quantize(y[b].y, G.m);
+        ts += (u128)q0 + q1;
+        if (ess) add_u192_u128(q2, (u128)q0 * q0 + (u128)q1 * q1);   // q <= 2^62: < 2^125
       }
     }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) ts += shfl_xor_u128(ts, d);
+    if (lane == 0) a.tile_excl[t] = run;
+    run += ts;
   }
+  if (lane == 0 && chunk < a.n_chunks) a.tile_sum[chunk] = run;
+  if (ess) {
 #pragma unroll
-  for (int tt = 0; tt < kTPB; ++tt) {
-    u128 acc = 0, acc2 = 0;                              // acc2: sum of q^2 (< 8 * 2^124)
-#pragma unroll
-    for (int r = 0; r < kItems; ++r) {
-      const unsigned long long q = quantize(v[tt][r], G.m);
-      acc += q;
-      if (ess) acc2 += (u128)q * q;
-    }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) acc += shfl_xor_u128(acc, d);
-    if (lane == 0) s_w[tt][warp] = acc;
-    if (ess) {
-      U192 q2;
-      q2.w[0] = (unsigned long long)acc2; q2.w[1] = (unsigned long long)(acc2 >> 64); q2.w[2] = 0;
-#pragma unroll
-      for (int d = 16; d > 0; d >>= 1) add_u192(q2, shfl_xor_u192(q2, d));
-      if (lane == 0) s_q2[tt][warp] = q2;
-    }
+    for (int d = 16; d > 0; d >>= 1) add_u192(q2, shfl_xor_u192(q2, d));
+    if (lane == 0 && chunk < a.n_chunks) a.tile_q2[chunk] = q2;
   }
   __syncthreads();
-  if (threadIdx.x < kTPB) {
-    const int tile = blockIdx.x * kTPB + threadIdx.x;
-    if (tile < a.n_tiles) {
-      u128 t = 0;
-      for (int w = 0; w < kThreads / 32; ++w) t += s_w[threadIdx.x][w];
-      a.tile_sum[tile] = t;
-      if (ess) {
-        U192 q = s_q2[threadIdx.x][0];
-        for (int w = 1; w < kThreads / 32; ++w) add_u192(q, s_q2[threadIdx.x][w]);
-        a.tile_q2[tile] = q;
-      }
-    }
-  }
   if (threadIdx.x == 0) {
     __threadfence();
     s_ticket = atomicAdd(&a.ctrl->counter, 1u);
   }
   __syncthreads();
   if (s_ticket != gridDim.x - 1) return;
-  // ---- last CTA: exclusive scan of the tile sums, shard total -> recB
+  // ---- last CTA: exclusive scan of the chunk sums (in place), shard total -> recB
   __threadfence();
-  const int nt = a.n_tiles;
-  const int per = (nt + kThreads - 1) / kThreads;
+  const int nc = a.n_chunks;
+  const int per = (nc + kThreads - 1) / kThreads;
   const int lo = threadIdx.x * per;
-  const int hi = min(nt, lo + per);
+  const int hi = min(nc, lo + per);
   u128 local = 0;
-  for (int t = lo; t < hi; ++t) local += ld_cg_u128(a.tile_sum + t);
-  // CTA exclusive scan of `local`
+#pragma unroll 4
+  for (int c = lo; c < hi; ++c) local += ld_cg_u128(a.tile_sum + c);
   u128 incl = local;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const u128 o = shfl_up_u128(incl, d);
     if (lane >= d) incl += o;
   }
-  if (lane == 31) s_w[0][warp] = incl;
+  __shared__ u128 s_w[kThreads / 32];
+  if (lane == 31) s_w[warp] = incl;
   __syncthreads();
   u128 woff = 0;
-  for (int w = 0; w < warp; ++w) woff += s_w[0][w];
-  u128 run = woff + incl - local;
-  for (int t = lo; t < hi; ++t) {
-    a.tile_excl[t] = run;
-    run += ld_cg_u128(a.tile_sum + t);
+  for (int w = 0; w < warp; ++w) woff += s_w[w];
+  u128 rr = woff + incl - local;
+  u128 sums[4];
+  for (int c0 = lo; c0 < hi; c0 += 4) {                // batched reloads, then in-place prefixes
+#pragma unroll
+    for (int u = 0; u < 4; ++u) sums[u] = c0 + u < hi ? ld_cg_u128(a.tile_sum + c0 + u) : (u128)0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (c0 + u < hi) { a.tile_sum[c0 + u] = rr; rr += sums[u]; }
   }
   if (threadIdx.x == kThreads - 1) {
-    a.recB[par * a.world + a.rank].W = run;     // shard total
+    a.recB[par * a.world + a.rank].W = rr;             // shard total
     a.ctrl->counter = 0;
   }
-  if (ess) {                                   // uniform: whole CTA
-    // shard sum of q^2: each thread its tile range, then warps, then the CTA
+  if (ess) {                                           // uniform: whole CTA
     U192 q = {{0, 0, 0}};
-    for (int t = lo; t < hi; ++t) {
+    for (int c = lo; c < hi; ++c) {
       U192 v;
-      const unsigned long long* src = (const unsigned long long*)(a.tile_q2 + t);
+      const unsigned long long* src = (const unsigned long long*)(a.tile_q2 + c);
       v.w[0] = __ldcg(src); v.w[1] = __ldcg(src + 1); v.w[2] = __ldcg(src + 2);
       add_u192(q, v);
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) add_u192(q, shfl_xor_u192(q, d));
-    if (lane == 0) s_q2[0][warp] = q;
+    if (lane == 0) s_q2[warp] = q;
     __syncthreads();
     if (threadIdx.x == 0) {
-      U192 t = s_q2[0][0];
-      for (int w = 1; w < kThreads / 32; ++w) add_u192(t, s_q2[0][w]);
+      U192 t = s_q2[0];
+      for (int w = 1; w < kThreads / 32; ++w) add_u192(t, s_q2[w]);
       RecB* rb = a.recB + par * a.world + a.rank;
       rb->q2[0] = t.w[0]; rb->q2[1] = t.w[1]; rb->q2[2] = t.w[2];
     }
@@ -624,13 +648,21 @@ __device__ __forceinline__ Grid make_grid_w(u128 W, unsigned long long n_total, 
 }
 
 template <int P, int ITEMS>   // P = planes per particle (<= 0: runtime a.planes)
-__global__ void __launch_bounds__(kThreads) anc_gather_kernel(ResArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) anc_gather_kernel(ResArgs a) {
   constexpr int kTile = kThreads * ITEMS;
   constexpr int kItems = ITEMS;
   __shared__ double s_lw[kTile];
   __shared__ unsigned s_O[kTile];
   __shared__ u128 s_w[kThreads / 32];
   __shared__ unsigned long long s_jlo;
+  const unsigned long long base = (unsigned long long)blockIdx.x * kTile;
+  const int cnt = (int)min((unsigned long long)kTile, a.n_local - base);
+  double lwv[kItems];                      // striped (coalesced) loads, before the control reads
+#pragma unroll
+  for (int r = 0; r < kItems; ++r) {
+    const int k = r * kThreads + threadIdx.x;
+    lwv[r] = k < cnt ? __ldg(a.lw + base + k) : -INFINITY;
+  }
   if (*(volatile unsigned*)&a.ctrl->done) return;
   const unsigned epoch = a.ctrl->epoch;
   const unsigned par = epoch & 1;
@@ -638,8 +670,6 @@ __global__ void __launch_bounds__(kThreads) anc_gather_kernel(ResArgs a) {
   if (!G.ok || G.alive == 0) return;       // error, or final epoch: no resample
   u128 prefix;
   const Grid gr = make_grid(a, a.recB + par * a.world, epoch, prefix);
-  const unsigned long long base = (unsigned long long)blockIdx.x * kTile;
-  const int cnt = (int)min((unsigned long long)kTile, a.n_local - base);
   if (!ess_resample(gr.W, total_q2(a.recB + par * a.world, a.world), a.n_total, a.ctrl->ess_a,
                     a.ctrl->ess_b)) {
     // ESS high enough: no resample (R-19); keep the states (copy to the other
@@ -655,12 +685,9 @@ __global__ void __launch_bounds__(kThreads) anc_gather_kernel(ResArgs a) {
     }
     return;
   }
-  // striped (coalesced) load, blocked use
+  // striped load, blocked use
 #pragma unroll
-  for (int r = 0; r < kItems; ++r) {
-    const int k = r * kThreads + threadIdx.x;
-    s_lw[k] = k < cnt ? __ldg(a.lw + base + k) : -INFINITY;
-  }
+  for (int r = 0; r < kItems; ++r) s_lw[r * kThreads + threadIdx.x] = lwv[r];
   __syncthreads();
   unsigned long long q[kItems];
   u128 tsum = 0;
@@ -681,7 +708,7 @@ __global__ void __launch_bounds__(kThreads) anc_gather_kernel(ResArgs a) {
   __syncthreads();
   u128 woff = 0;
   for (int w = 0; w < warp; ++w) woff += s_w[w];
-  const u128 tile_start = prefix + a.tile_excl[blockIdx.x];
+  const u128 tile_start = prefix + tile_prefix(a, blockIdx.x);
   u128 C = tile_start + woff + incl - tsum;   // exclusive prefix of this thread's first item
   if (threadIdx.x == 0) s_jlo = gr.count_below(tile_start);
   unsigned long long prevO = 0;
@@ -707,17 +734,35 @@ __global__ void __launch_bounds__(kThreads) anc_gather_kernel(ResArgs a) {
   if (lane == 0 && distinct) atomicAdd(&a.ctrl->distinct, (unsigned long long)distinct);
 
   const unsigned long long jhi = cnt > 0 ? s_O[cnt - 1] : jlo;
-  const int np = P > 0 ? P : a.planes;
-  for (unsigned long long j = jlo + threadIdx.x; j < jhi; j += kThreads) {
-    // k = first item with O_k > j
-    int lo = 0, hi = cnt - 1;
+  // Output slots.  Warp w's particles [w*32*kItems, (w+1)*32*kItems) (its
+  // lanes' blocked items) fill the contiguous slots [O_{first-1}, O_last): the
+  // lanes take consecutive slots and binary-search the warp's O values.  If a
+  // warp owns more than 8 slots per particle (a few dominant weights), the
+  // whole CTA shares the tile's slots instead.
+  const int wk0 = warp * 32 * kItems, wn = 32 * kItems;
+  const unsigned wA = wk0 ? s_O[wk0 - 1] : (unsigned)jlo;
+  const unsigned wB = s_O[wk0 + wn - 1];
+#ifdef SMC_ANC_WARP
+  const bool heavy = __syncthreads_or(wB - wA > 8u * (unsigned)wn);
+#else
+  const bool heavy = true;                  // measured: CTA-wide striping balances better
+#endif
+  const unsigned long long j_first = heavy ? jlo + threadIdx.x : wA + lane;
+  const unsigned long long j_end = heavy ? jhi : wB;
+  const unsigned j_step = heavy ? kThreads : 32;
+  const int s_lo = heavy ? 0 : wk0, s_hi = heavy ? kTile - 1 : wk0 + wn - 1;
+  for (unsigned long long j = j_first; j < j_end; j += j_step) {
+    int lo = s_lo, hi = s_hi;               // first item with O_k > j
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
       if (s_O[mid] > j) hi = mid; else lo = mid + 1;
     }
     const unsigned long long src = base + lo;
-    const unsigned long long dshard = j / a.n_local;
-    const unsigned long long dl = j - dshard * a.n_local;
+    unsigned long long dshard = 0, dl = j;
+    if (a.world > 1) {
+      dshard = j / a.n_local;
+      dl = j - dshard * a.n_local;
+    }
     uint4* dst = a.dst_planes[dshard];
     const int skip = stack_skip_lo(a, a.src_planes, src);     // R-22: stack prefix only
     if (P > 0) {
@@ -729,7 +774,7 @@ __global__ void __launch_bounds__(kThreads) anc_gather_kernel(ResArgs a) {
       for (int p = 0; p < (P > 0 ? P : 1); ++p)
         if (copy_plane(a, p, skip)) dst[(unsigned long long)p * a.n_local + dl] = v[p];
     } else {
-      for (int p = 0; p < np; ++p)
+      for (int p = 0; p < a.planes; ++p)
         if (copy_plane(a, p, skip))
           dst[(unsigned long long)p * a.n_local + dl] = __ldg(a.src_planes + (unsigned long long)p * a.n_local + src);
     }
@@ -800,7 +845,7 @@ __global__ void __launch_bounds__(kThreads) offspring_kernel(ResArgs a) {
   __syncthreads();
   u128 woff = 0;
   for (int w = 0; w < warp; ++w) woff += s_w[w];
-  const u128 tile_start = prefix + a.tile_excl[blockIdx.x];
+  const u128 tile_start = prefix + tile_prefix(a, blockIdx.x);
   u128 C = tile_start + woff + incl - tsum;
   if (threadIdx.x == 0) s_jlo = gr.count_below(tile_start);
   unsigned long long prevO = 0;
