@@ -303,13 +303,17 @@ def bench_sweeps(args, wl, smc, torch, world, rank):
         res_bytes += st["resamples"] * n_loc * (20 + sb) + sb * st["distinct"] + 8 * n_loc
         n_resamples += st["resamples"]
     h.set_timing(False)
-    # graph body = 2 epochs x (propagate, reduce, anc_gather, finalize) + set_condition
+    # graph body = 2 epochs x (propagate + resampling) + set_condition; the
+    # resampling step is one cooperative launch when the handle uses the fused
+    # kernel (resample_grid() > 0), else reduce, anc_gather, finalize
+    fused = world == 1 and h.resample_grid() > 0
+    per_epoch = 2 if fused else 4
     E = steps_done // args.steps
-    launches = args.steps * 9 * ((E + 1) // 2)
+    launches = args.steps * (2 * per_epoch + 1) * ((E + 1) // 2)
     return dict(h=h, model=model, N=N, t_ms=t_ms, value=value, sweeps=sweeps_per_s, prop_ms=prop_ms,
                 res_bytes=res_bytes, resamples_per_sweep=n_resamples / args.steps,
                 res_ms=res_ms, draws=draws, alive_steps=alive_steps, epochs=steps_done,
-                launches=launches, clocks=clk.summary(torch.cuda.current_device()),
+                launches=launches, fused=fused, clocks=clk.summary(torch.cuda.current_device()),
                 logz=float(np.mean(logzs)))
 
 
@@ -541,8 +545,10 @@ def run_ours(args, wl):
                 resample_roofline=dict(bound="hbm", achieved=r["res_bytes"] / (r["res_ms"] * 1e-3) / 1e9,
                                        peak=hbm_peak, unit="GB/s",
                                        frac=r["res_bytes"] / (r["res_ms"] * 1e-3) / 1e9 / hbm_peak,
-                                       note="reduce + anc_gather + finalize per epoch at this N "
-                                            "(latency-bound at 10^6; see workload 'resample')"),
+                                       kernel=("resample_fused_kernel (one cooperative launch per epoch)"
+                                               if r["fused"] else "reduce + anc_gather + finalize"),
+                                       note="per epoch at this N (latency-bound at 10^6; "
+                                            "see workload 'resample' for the HBM-bound sizes)"),
                 roofline=dict(bound="alu",
                               kernel=("propagate_lr_kernel" if args.rng == "lineage" and wl["model"] in ("crbd", "clads2")
                                       and not wl.get("analytic") else "propagate_kernel") + f"<{args.workload}>",
