@@ -23,6 +23,10 @@ runs = [
     ("crbd-lr-inplace", smc.Model.crbd(t90, lineage=True, flags=smc.FLAG_INPLACE), 700),
     ("clads2-lr-inplace", smc.Model.clads2(t5, lineage=True, flags=smc.FLAG_INPLACE), 500),
     ("ssm-inplace", smc.Model.ssm(inputs.ssm_series(10), flags=smc.FLAG_INPLACE), 600),
+    # several CTAs of the fused resampling kernel (grid barrier, ragged last block)
+    ("crbd-lr-fused-20k", smc.Model.crbd(t90, lineage=True), 20000),
+    # peaked likelihood: dominant weights take the CTA-wide (heavy) slot path
+    ("ssm-peaked-fused", smc.Model(smc.SSM, inputs.ssm_series(10), [0.0, 100.0, 2.0, 1.0, 1e-4]), 20000),
 ]
 modes = (False,) if "--step-only" in sys.argv else (False, True)
 if "--shards-first" in sys.argv:
@@ -34,7 +38,7 @@ for name, m, n in runs:
     for graph in modes:
         h = smc.Smc(m, n, 3, shards=1)
         h.set_graph(graph)
-        if "analytic" in name or "ssm" in name:
+        if "analytic" in name or ("ssm" in name and "peaked" not in name):
             h.set_ess_threshold(1, 2)             # ESS path (R-19): Sum q^2, identity copies
         rc = h.run_status()
         print(name, "graph" if graph else "step", rc, h.log_z)
