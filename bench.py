@@ -422,6 +422,7 @@ def bench_resample(args, wl, smc, torch):
     ms_k = [v / args.steps for v in r.stats()["ms_kernel"]]
     r.set_timing(False)
     return dict(r=r, n=n, t_ms=float(np.mean(times)), alg_bytes=alg, D=D, ms_kernel=ms_k,
+                fused=r.resample_grid() > 0,
                 clocks=clk.summary(torch.cuda.current_device()))
 
 
@@ -484,6 +485,9 @@ def run_ours(args, wl):
         n, D = r["n"], r["D"]
         g_bytes = n * 12 + 64 * (D + n)          # anc_gather: lw read, anc write, states
         kname = "anc_gather_kernel (ancestors + fused gather)"
+        fused = r["fused"]
+        if fused:                                # N fits the co-resident grid: one launch
+            kname = "resample_fused_kernel (quantise + exact sum, grid barrier, ancestors + gather, log Z)"
         metric = "resample effective HBM GB/s (B_alg = N*20 + 64*(D+N))"
         if args.inplace:
             # offspring: lw 8 + O_k 4; permute: O_k 4 + survivors' anc 4 D + hole/extra
@@ -509,12 +513,14 @@ def run_ours(args, wl):
                                   algorithmic_bytes=g_bytes, ms=g_ms, peak_source=pk_kind),
                     chain_roofline=dict(bound="hbm", achieved=achieved, peak=hbm_peak, unit="GB/s",
                                         frac=achieved / hbm_peak, algorithmic_bytes=r["alg_bytes"],
-                                        note="max + reduce + anc_gather + finalize; B_alg excludes "
-                                             "the standalone max pass (8 B/particle)"),
-                    kernel_ms=dict(zip(["max", "reduce", "inplace_chain" if args.inplace else "anc_gather",
-                                        "finalize"], r["ms_kernel"])),
+                                        note=("max + resample_fused" if fused else
+                                              "max + reduce + anc_gather + finalize") +
+                                             "; B_alg excludes the standalone max pass (8 B/particle)"),
+                    kernel_ms=(dict(max=r["ms_kernel"][0], resample_fused=r["ms_kernel"][2]) if fused else
+                               dict(zip(["max", "reduce", "inplace_chain" if args.inplace else "anc_gather",
+                                         "finalize"], r["ms_kernel"]))),
                     distinct_ancestors=D,
-                    gpu_launches=(7 if args.inplace else 5) * args.steps, clocks=r["clocks"])
+                    gpu_launches=(7 if args.inplace else 3 if fused else 5) * args.steps, clocks=r["clocks"])
         if rank == 0:
             print(json.dumps(line), flush=True)
         return

@@ -380,6 +380,12 @@ class Resampler:
         _check(self.h, _lib.smc_last_distinct(self.h, C.byref(v)))
         return v.value
 
+    def resample_grid(self):
+        """CTAs of the single-launch fused resampling step (0: split kernels)."""
+        v = C.c_int32(0)
+        _check(self.h, _lib.smc_resample_grid(self.h, C.byref(v)))
+        return v.value
+
 
 def plan_ranges(shard_totals, n_per: int, z: int):
     """Output slot range of each shard for integer shard totals (Python ints)

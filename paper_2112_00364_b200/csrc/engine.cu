@@ -414,8 +414,7 @@ const void* fused_fn(int planes) {
 int plan_fused(smc_ctx* h) {
   h->fused_grid = 0;
   const char* off = std::getenv("SMC_NO_FUSED_RESAMPLE");
-  if ((off && off[0] == '1') || h->world != 1 || h->n_local_shards != 1 || h->inplace ||
-      h->kind == SMC_RESAMPLE_BENCH)
+  if ((off && off[0] == '1') || h->world != 1 || h->n_local_shards != 1 || h->inplace)
     return SMC_OK;
   int dev = 0, sms = 0, optin = 0;
   CU(cudaGetDevice(&dev));
@@ -1277,12 +1276,22 @@ int smc_resample_device(smc_handle h, const double* d_lw, const void* d_state_in
   max_kernel<<<mgrid, kThreads, 0, h->stream>>>(d_lw, h->n_per, h->d_recA, 1, 0, s.ctrl);
   if (h->timing) CU(cudaEventRecord(h->rev[1], h->stream));
   ResArgs a = res_args(h, s, d_lw, (const uint4*)d_state_in, 1);
-  launch_reduce(h, a);
-  if (h->timing) CU(cudaEventRecord(h->rev[2], h->stream));
-  launch_resample_tail(h, a);
-  if (h->timing) CU(cudaEventRecord(h->rev[3], h->stream));
-  launch_finalize(h, s);
-  if (h->timing) CU(cudaEventRecord(h->rev[4], h->stream));
+  if (h->fused_grid > 0) {
+    // one cooperative launch: quantise + sum, grid barrier, ancestors + gather,
+    // log Z (timed in the anc_gather slot; reduce and finalize slots stay 0)
+    if (h->timing) CU(cudaEventRecord(h->rev[2], h->stream));
+    int rc = launch_fused(h, s, a);
+    if (rc) return rc;
+    if (h->timing) CU(cudaEventRecord(h->rev[3], h->stream));
+    if (h->timing) CU(cudaEventRecord(h->rev[4], h->stream));
+  } else {
+    launch_reduce(h, a);
+    if (h->timing) CU(cudaEventRecord(h->rev[2], h->stream));
+    launch_resample_tail(h, a);
+    if (h->timing) CU(cudaEventRecord(h->rev[3], h->stream));
+    launch_finalize(h, s);
+    if (h->timing) CU(cudaEventRecord(h->rev[4], h->stream));
+  }
   CU(cudaGetLastError());
   h->started = true;
   if (h->timing) {

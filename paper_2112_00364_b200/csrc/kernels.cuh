@@ -1383,7 +1383,11 @@ __global__ void __launch_bounds__(kFT, SMC_FUSED_MINB) resample_fused_kernel(Res
   const int wk0 = warp * 32 * ipt, wn = 32 * ipt;       // the warp's particles
   const unsigned wA = wk0 ? s_O[wk0 - 1] : s_O[blk];
   const unsigned wB = s_O[wk0 + wn - 1];
+#ifdef SMC_FUSED_CTA_STRIPE
+  if (threadIdx.x == 0) s_heavy = 1u;
+#else
   if (lane == 0 && wB - wA > kHeavy * (unsigned)wn) atomicOr(&s_heavy, 1u);
+#endif
   __syncthreads();
   if (!s_heavy) {
     // U chunks of 32 slots per iteration: U independent searches, then all

@@ -164,3 +164,53 @@ def test_fused_rejected_and_large_n_fallback(smc):
     big.run()
     # K = 4 checkpoints of weight 3 each: log Z = 4 ln 3 exactly up to rounding
     assert big.log_z == pytest.approx(4 * np.log(3.0), rel=1e-14)
+
+
+def _resampler(smc, N, S, seed, fused):
+    old = os.environ.pop("SMC_NO_FUSED_RESAMPLE", None)
+    if not fused:
+        os.environ["SMC_NO_FUSED_RESAMPLE"] = "1"
+    try:
+        r = smc.Resampler(N, S, seed=seed)
+    finally:
+        os.environ.pop("SMC_NO_FUSED_RESAMPLE", None)
+        if old is not None:
+            os.environ["SMC_NO_FUSED_RESAMPLE"] = old
+    assert (r.resample_grid() > 0) == fused
+    return r
+
+
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "split"])
+@pytest.mark.parametrize("N,S,sigma,finf", [(1, 64, 0.0, 0.0), (2049, 64, 1.0, 0.0),
+                                            (100_003, 64, 4.0, 0.25), (300_001, 32, 12.0, 0.5),
+                                            (40_000, 272, 2.0, 0.1)])
+def test_resampler_both_paths_vs_oracle(smc, fused, N, S, sigma, finf):
+    """configs[4] resampling step on the fused and the split path against the
+    oracle: ancestors and gathered states bit-exact, log Z increment."""
+    lw = inputs.resample_lw(N, sigma, finf, seed=N + 7)
+    if not np.isfinite(lw).any():
+        lw[0] = 0.0
+    st = inputs.state_bytes(N, S, seed=N + 8)
+    r = _resampler(smc, N, S, 78, fused)
+    for epoch in (0, 3):
+        anc, out, inc = r.host(lw, smc.aos_to_soa(st), epoch=epoch)
+        ref = oracle.resample(lw, seed=78, epoch=epoch)
+        np.testing.assert_array_equal(anc, ref["anc"])
+        assert inc == pytest.approx(ref["logz_inc"], rel=1e-13, abs=1e-13)
+        np.testing.assert_array_equal(smc.soa_to_aos(out), oracle.gather(st, ref["anc"]))
+        assert r.distinct() == len(np.unique(ref["anc"]))
+
+
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "split"])
+def test_resampler_one_dominant_weight(smc, fused):
+    """All offspring to one particle (the heavy slot path)."""
+    N = 200_000
+    lw = np.full(N, -np.inf)
+    lw[123_457] = 0.0
+    lw[5] = -50.0                     # quantises to 0: no offspring
+    st = inputs.state_bytes(N, 32, seed=9)
+    r = _resampler(smc, N, 32, 5, fused)
+    anc, out, inc = r.host(lw, smc.aos_to_soa(st), epoch=1)
+    assert (anc == 123_457).all()
+    np.testing.assert_array_equal(smc.soa_to_aos(out), oracle.gather(st, anc))
+    assert inc == pytest.approx(-np.log(N), rel=1e-14)
