@@ -317,7 +317,7 @@ __device__ __forceinline__ void propagate_one(const PropArgs& a, const ModelCons
 }
 
 // Register cap per model (M::kMinBlocks resident CTAs per SM), measured on
-// B200: CRBD 4 (64 regs), SEIR 3 (80 regs; samplers out of line), ClaDS2 2.
+// B200: CRBD 4 (64 regs), SEIR 4 (64 regs, samplers out of line; 3 CTAs at 80 regs measured 1.7% slower), ClaDS2 2.
 // Grid (M::kOneWave): light models run one wave of resident CTAs and
 // grid-stride, so the epilogue's same-address atomics run once per CTA;
 // uneven models run one particle per thread and let the block scheduler

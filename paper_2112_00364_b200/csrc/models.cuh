@@ -344,9 +344,12 @@ struct Clads2 {
 // Planes: P0 {lam_h, del_h} P1 {gam_h, lam_m} P2 {del_m, rho}
 //         P3 {sh, eh, ih, rh} P4 {sm, em, im, t} P5 {pc, 0, 0, 0}.
 // ============================================================================
+#ifndef SMC_SEIR_MINB
+#define SMC_SEIR_MINB 4   // 64 registers (some spills): 86.9 vs 88.5 ms/sweep at 3 (80 registers)
+#endif
 struct Seir {
   static constexpr int kPlanes = 6;
-  static constexpr int kMinBlocks = 3;
+  static constexpr int kMinBlocks = SMC_SEIR_MINB;
   static constexpr bool kOneWave = false;  // grid: one CTA per 256 particles (uneven work: block scheduler balances)
   struct State { double lam_h, del_h, gam_h, lam_m, del_m, rho; int sh, eh, ih, rh, sm, em, im, t, pc; };
   __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
