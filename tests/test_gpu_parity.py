@@ -244,6 +244,19 @@ def test_crbd_full_size_prefix(smc, ck):
              per_epoch=True, max_epochs=4)
 
 
+@CLADS_K
+def test_clads2_full_size_prefix(smc, ck):
+    """BASELINE configs[2] on one GPU (10^6 particles), first 3 epochs, element
+    by element (log-weights, ancestors, every state field)."""
+    run_pair(smc, ck, inputs.tree("tree90"), inputs.CLADS2_PARAMS, 1_000_000, 2,
+             per_epoch=True, max_epochs=3)
+
+
+def test_seir_full_size_prefix(smc):
+    """BASELINE configs[3] (10^6 particles, the 182-day series), first 3 epochs."""
+    run_pair(smc, oracle.SEIR, inputs.seir_series(), None, 1_000_000, 3, per_epoch=True, max_epochs=3)
+
+
 # ------------------------------------------------------------- whole-run CUDA graph
 @pytest.mark.parametrize("kind,data,params,N", [
     (oracle.CRBD, "tree90", inputs.CRBD_PARAMS, 5000),
