@@ -425,7 +425,7 @@ int plan_fused(smc_ctx* h) {
   if (!coop) return SMC_OK;
   const void* fn = fused_fn(h->planes);
   const unsigned long long n = h->n_per;
-  for (int per_sm : {2, 1}) {
+  for (int per_sm = SMC_FUSED_MINB; per_sm >= 1; --per_sm) {
     const unsigned long long g0 = (unsigned long long)sms * per_sm;
     const unsigned long long ipt = std::max(1ull, (n + g0 * kFT - 1) / (g0 * kFT));
     const size_t smem = (size_t)ipt * kFT * 12 + 4;      // q and O_k per particle

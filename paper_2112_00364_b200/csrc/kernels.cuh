@@ -1167,7 +1167,10 @@ __global__ void __launch_bounds__(kThreads) max_kernel(const double* lw, unsigne
 // launch replaces reduce + anc_gather + finalize.  Results are identical to
 // the split path (same integers, same grid, same slot ownership).
 // ============================================================================
-constexpr int kFT = 512;                 // threads per fused CTA
+#ifndef SMC_FUSED_THREADS
+#define SMC_FUSED_THREADS 512
+#endif
+constexpr int kFT = SMC_FUSED_THREADS;   // threads per fused CTA
 #ifndef SMC_FUSED_MINB
 #define SMC_FUSED_MINB 2                 // resident CTAs per SM (register cap 64)
 #endif
