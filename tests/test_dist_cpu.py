@@ -50,3 +50,26 @@ def test_gloo_world2_host_exchanges(tmp_path):
     assert r0[3] == 0 and r1[3] == 0
     assert r0[2] == [1] * 16 + [2] * 16 == r1[2]       # callback concatenates in rank order
     assert r0[4] == r1[4]                              # broadcast NCCL id (or the same error)
+
+
+def test_reference_arm_under_torchrun_world2():
+    """bench.py --impl reference launched like the driver's N=2 run: rank 0 alone
+    times the oracle and prints ONE JSON line; rank 1 exits 0 without work."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--impl", "reference",
+           "--gpus", "2", "--steps", "1", "--warmup", "0", "--cpu-budget", "1"]
+    p = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] == 0
