@@ -266,7 +266,9 @@ const char* smc_errmsg(smc_handle h);
  * ancestors.  `epoch` selects the resampling uniform (Philox counter
  * (0, epoch, 0, 1)).  Enqueued on the handle's stream, no synchronisation.
  * Reads back the log Z increment into *logz_inc only if logz_inc != NULL
- * (synchronises). */
+ * (synchronises).  d_lw, d_state_in and d_state_out must be 16-byte aligned
+ * (128-bit loads/stores; SMC_EINVAL otherwise).  The caller's pointers are
+ * used for this call only (the handle's own buffers are not redirected). */
 int smc_resample_device(smc_handle h, const double* d_lw, const void* d_state_in,
                         void* d_state_out, uint32_t* d_anc, uint32_t epoch, double* logz_inc);
 /* Same with HOST buffers: copies in, resamples, copies anc and states out

@@ -18,6 +18,8 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -90,6 +92,7 @@ struct smc_ctx {
   int fused_grid = 0;             // > 0: single-shard resampling in one cooperative launch
   int fused_ipt = 0;              // particles per thread of resample_fused_kernel
   size_t fused_smem = 0;
+  void** d_call_tab = nullptr;    // smc_resample_device: {state_out, anc} of the current call
   u128* d_blk_sum = nullptr;      // [fused_grid]
   U192* d_blk_q2 = nullptr;       // [fused_grid]
   bool stack_prefix = true;       // §R-22 copy only the used stack prefix (env SMC_NO_STACK_PREFIX=1: off, diagnostics)
@@ -176,16 +179,23 @@ bool parse_tree(const double* d, uint64_t len, TreeIn& T, std::string& err) {
     T.right[i] = (int)d[4 + 4 * i];
     T.age[i] = d[5 + 4 * i];
     const bool tip = T.left[i] < 0;
-    if (tip != (T.right[i] < 0) || T.left[i] >= T.M || T.right[i] >= T.M) {
+    if (tip != (T.right[i] < 0) || T.left[i] >= T.M || T.right[i] >= T.M ||
+        T.parent[i] >= T.M || (T.parent[i] < 0) != (i == T.root)) {
       err = "malformed tree node";
       return false;
     }
   }
   if (T.left[T.root] < 0) { err = "root must be internal"; return false; }
-  // tip counts by an explicit post-order (iterative)
+  for (int v = 0; v < T.M; ++v)      // child pointers and parent pointers agree
+    if (T.left[v] >= 0 && (T.parent[T.left[v]] != v || T.parent[T.right[v]] != v)) {
+      err = "tree parent/child pointers disagree";
+      return false;
+    }
+  // tip counts by an explicit post-order (iterative; a cycle stops it at M nodes)
   T.tips.assign(T.M, 0);
   std::vector<int> order, st{T.root};
   while (!st.empty()) {
+    if ((int)order.size() >= T.M) { err = "tree is not connected / has cycles"; return false; }
     int v = st.back(); st.pop_back();
     order.push_back(v);
     if (T.left[v] >= 0) { st.push_back(T.left[v]); st.push_back(T.right[v]); }
@@ -411,6 +421,19 @@ const void* fused_fn(int planes) {
     default: return (const void*)resample_fused_kernel<0>;
   }
 }
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per kernel and process-wide:
+// only ever raise it, so a later, smaller handle cannot lower the cap below
+// what an earlier handle's launches request.
+cudaError_t raise_smem_cap(const void* fn, size_t smem) {
+  static std::mutex mu;
+  static std::map<const void*, size_t> cap;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& c = cap[fn];
+  if (smem <= c) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) c = smem;
+  return e;
+}
 int plan_fused(smc_ctx* h) {
   h->fused_grid = 0;
   const char* off = std::getenv("SMC_NO_FUSED_RESAMPLE");
@@ -430,7 +453,7 @@ int plan_fused(smc_ctx* h) {
     const unsigned long long ipt = std::max(1ull, (n + g0 * kFT - 1) / (g0 * kFT));
     const size_t smem = (size_t)ipt * kFT * 12 + 4;      // q and O_k per particle
     if (smem + 8192 > (size_t)optin) continue;
-    CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CU(raise_smem_cap(fn, smem));
     int nb = 0;
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, kFT, smem));
     if (nb < per_sm) continue;
@@ -829,6 +852,13 @@ int build_graph(smc_ctx* h) {
   return SMC_OK;
 }
 
+void drop_graph(smc_ctx* h) {
+  if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
+  if (h->graph) cudaGraphDestroy(h->graph);
+  h->graph_exec = nullptr;
+  h->graph = nullptr;
+}
+
 int read_ctrl(smc_ctx* h) {
   CU(cudaMemcpyAsync(h->h_ctrl, h->shards[0].ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->stream));
   CU(cudaStreamSynchronize(h->stream));
@@ -1012,7 +1042,7 @@ void smc_destroy(smc_handle h) {
     cudaFree(s.scratch);
   }
   cudaFree(h->d_table); cudaFree(h->d_logfact); cudaFree(h->d_recA); cudaFree(h->d_recB); cudaFree(h->d_barrier);
-  cudaFree(h->d_blk_sum); cudaFree(h->d_blk_q2);
+  cudaFree(h->d_blk_sum); cudaFree(h->d_blk_q2); cudaFree(h->d_call_tab);
   cudaFree(h->tasks.sid); cudaFree(h->tasks.lam); cudaFree(h->tasks.owner);
   if (h->graph_exec) cudaGraphExecDestroy(h->graph_exec);
   if (h->graph) cudaGraphDestroy(h->graph);
@@ -1060,7 +1090,12 @@ int smc_set_data(smc_handle h, const double* data, uint64_t data_len) {
   int rc = setup_model(h, &m);
   const double derived_p5 = h->mc.p[5];          // ClaDS2: root child order of the NEW tree
   std::memcpy(h->mc.p, saved_p, sizeof(saved_p));
-  if (h->kind == SMC_CLADS2) h->mc.p[5] = derived_p5;
+  if (h->kind == SMC_CLADS2 && rc == SMC_OK && derived_p5 != saved_p[5]) {
+    // the root child order is a kernel argument captured by value in the
+    // whole-run graph: recapture it (stale ModelConst)
+    h->mc.p[5] = derived_p5;
+    drop_graph(h);
+  }
   if (rc == SMC_OK && (h->mc.n != old_n || h->h_table.size() != old.size()))
     rc = fail(h, SMC_EINVAL, "new data must have the same shape");
   if (rc != SMC_OK) {
@@ -1126,6 +1161,32 @@ int smc_step(smc_handle h, int32_t* done) {
 int smc_run(smc_handle h) {
   int rc = check_ready(h);
   if (rc) return rc;
+  if (h->comm == COMM_NCCL && !h->timing) {
+    // one process per GPU with NCCL records: NCCL calls stay out of the WHILE
+    // conditional graph.  The host enqueues kBatch epochs at a
+    // time and reads the device flag once per batch; epochs enqueued after the
+    // end are device no-ops, and every rank sees the same global `done`, so all
+    // ranks enqueue the same collectives.
+    constexpr int kBatch = 8;
+    h->started = true;
+    while (!h->h_ctrl->done) {
+      for (int k = 0; k < kBatch; ++k) {
+        rc = enqueue_epoch(h);
+        if (rc) return rc;
+      }
+      rc = read_ctrl(h);
+      if (rc) return rc;
+    }
+    h->enq = h->h_ctrl->epochs;
+    return status_of(*h->h_ctrl);
+  }
+  if (h->use_graph && !h->timing && h->comm != COMM_CALLBACK && !h->h_ctrl->done && (h->enq & 1)) {
+    // the graph body is captured as {even epoch, odd epoch}: after an odd
+    // number of smc_step calls take one host step to return to even parity
+    int32_t done = 0;
+    rc = smc_step(h, &done);
+    if (rc || done) return rc;
+  }
   if (h->use_graph && !h->timing && h->comm != COMM_CALLBACK && !h->h_ctrl->done) {
     // device-side epoch loop: one graph launch, one synchronisation
     rc = build_graph(h);
@@ -1265,17 +1326,23 @@ int smc_resample_device(smc_handle h, const double* d_lw, const void* d_state_in
   if (!d_lw || !d_state_in || !d_state_out || !d_anc) return fail(h, SMC_EINVAL, "NULL buffer");
   if (h->inplace && d_state_out != d_state_in)
     return fail(h, SMC_EINVAL, "SMC_FLAG_INPLACE: d_state_out must be NULL or d_state_in");
+  if (((uintptr_t)d_lw | (uintptr_t)d_state_in | (uintptr_t)d_state_out) & 15)
+    return fail(h, SMC_EINVAL, "device buffers must be 16-byte aligned");
   Shard& s = h->shards[0];
-  // destination tables point at the caller's buffers
-  uint4* dst = (uint4*)d_state_out;
-  CU(cudaMemcpyAsync(s.d_dst_planes[1], &dst, sizeof(dst), cudaMemcpyHostToDevice, h->stream));
-  CU(cudaMemcpyAsync(s.d_dst_anc, &d_anc, sizeof(d_anc), cudaMemcpyHostToDevice, h->stream));
+  // this call's destinations go through the handle's per-call pointer table
+  // (the shard's own destination tables stay untouched); pageable
+  // host sources are consumed before cudaMemcpyAsync returns
+  if (!h->d_call_tab) CU(cudaMalloc(&h->d_call_tab, 2 * sizeof(void*)));
+  void* tab[2] = {d_state_out, d_anc};
+  CU(cudaMemcpyAsync(h->d_call_tab, tab, sizeof(tab), cudaMemcpyHostToDevice, h->stream));
   prep_resample_kernel<<<1, 32, 0, h->stream>>>(s.ctrl, h->d_recA, h->d_recB, 1, 0, epoch);
   const unsigned mgrid = (unsigned)std::min<unsigned long long>((h->n_per + kThreads - 1) / kThreads, 148ull * 8);
   if (h->timing) CU(cudaEventRecord(h->rev[0], h->stream));
   max_kernel<<<mgrid, kThreads, 0, h->stream>>>(d_lw, h->n_per, h->d_recA, 1, 0, s.ctrl);
   if (h->timing) CU(cudaEventRecord(h->rev[1], h->stream));
   ResArgs a = res_args(h, s, d_lw, (const uint4*)d_state_in, 1);
+  a.dst_planes = reinterpret_cast<uint4* const*>(h->d_call_tab);
+  a.dst_anc = reinterpret_cast<uint32_t* const*>(h->d_call_tab + 1);
   if (h->fused_grid > 0) {
     // one cooperative launch: quantise + sum, grid barrier, ancestors + gather,
     // log Z (timed in the anc_gather slot; reduce and finalize slots stay 0)
@@ -1324,11 +1391,6 @@ int smc_resample_host(smc_handle h, const double* lw, const void* state_in, void
   CU(cudaMemcpyAsync(anc, s.anc, h->n_per * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream));
   CU(cudaMemcpyAsync(state_out, s.planes[1], sb, cudaMemcpyDeviceToHost, h->stream));
   CU(cudaStreamSynchronize(h->stream));
-  // restore the handle's own destination tables
-  uint4* p1 = s.planes[1];
-  uint32_t* an = s.anc;
-  CU(cudaMemcpy(s.d_dst_planes[1], &p1, sizeof(p1), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(s.d_dst_anc, &an, sizeof(an), cudaMemcpyHostToDevice));
   if (logz_inc) *logz_inc = inc;
   return SMC_OK;
 }

@@ -92,3 +92,38 @@ def gpu_resample_worker(rank, world, port, outdir, n_per):
     h.close()
     dist.barrier()
     dist.destroy_process_group()
+
+
+def gpu_nccl_worker(rank, world, port, outdir, n_per, seed):
+    """One process per GPU with comm="nccl" (the bench's multi-GPU path):
+    CRBD (both RNG readings) and ClaDS2-LR runs plus a configs[4] resampling
+    step; results saved for comparison with one process holding all particles."""
+    dist = init(rank, world, port)
+    import torch
+    torch.cuda.set_device(rank)
+    import inputs
+    import paper_2112_00364_b200 as smc
+    from paper_2112_00364_b200 import dist as sdist
+    t90 = inputs.tree("tree90")
+    out = {}
+    for name, m in (("crbd", smc.Model.crbd(t90)), ("crbd_lr", smc.Model.crbd(t90, lineage=True)),
+                    ("clads2_lr", smc.Model.clads2(t90, lineage=True))):
+        h = sdist.ShardedSmc(m, n_per, seed, comm="nccl")
+        rc = h.run_status()
+        out[name] = [rc, h.log_z, h.ancestors(), h.log_weights(), h.fields()]
+        h.close()
+    S = 64
+    N = world * n_per
+    lw = inputs.resample_lw(N, 2.0, 0.2, seed=41)[rank * n_per:(rank + 1) * n_per]
+    st = inputs.state_bytes(N, S, seed=42)[rank * n_per:(rank + 1) * n_per]
+    h = sdist.ShardedSmc(smc.Model.resample_bench(S), n_per, 7, comm="nccl")
+    h.load(lw, smc.aos_to_soa(st).ravel())
+    h.resample_step(0)
+    h.resample_step(1)
+    out["resample"] = [h.ancestors(), smc.soa_to_aos(h.state().reshape(S // 16, n_per, 16))]
+    h.close()
+    res = np.empty(1, dtype=object)
+    res[0] = out
+    np.save(os.path.join(outdir, f"n{rank}.npy"), res, allow_pickle=True)
+    dist.barrier()
+    dist.destroy_process_group()

@@ -42,3 +42,39 @@ def test_resample_two_processes_one_gpu(smc, tmp_path):
     a1 = oracle.resample(lw, seed=7, epoch=1)["anc"]
     np.testing.assert_array_equal(np.concatenate([r[0][0], r[1][0]]), a1)
     np.testing.assert_array_equal(np.concatenate([r[0][1], r[1][1]]), st[a0][a1])
+
+
+def _gpu_count():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+@pytest.mark.skipif(_gpu_count() < 2, reason="needs two CUDA devices (NCCL cannot put two ranks on one GPU)")
+def test_two_gpus_nccl_match_single(smc, tmp_path):
+    """comm="nccl" (records through NCCL, host-batched epoch loop, CUDA-IPC
+    peer stores over NVLink) is bit-identical to one process holding all
+    particles: CRBD (both RNG readings), ClaDS2-LR and a configs[4] step."""
+    import torch.multiprocessing as mp
+    import oracle
+    n_per, seed = 3000, 23
+    port = dist_workers.free_port()
+    mp.spawn(dist_workers.gpu_nccl_worker, args=(2, port, str(tmp_path), n_per, seed), nprocs=2, join=True)
+    r = [np.load(tmp_path / f"n{k}.npy", allow_pickle=True)[0] for k in range(2)]
+    t90 = inputs.tree("tree90")
+    for name, m in (("crbd", smc.Model.crbd(t90)), ("crbd_lr", smc.Model.crbd(t90, lineage=True)),
+                    ("clads2_lr", smc.Model.clads2(t90, lineage=True))):
+        ref = smc.Smc(m, 2 * n_per, seed)
+        assert ref.run_status() == r[0][name][0] == r[1][name][0] == smc.OK, name
+        assert r[0][name][1] == r[1][name][1] == ref.log_z, name
+        for k, get in ((2, ref.ancestors), (3, ref.log_weights), (4, ref.fields)):
+            np.testing.assert_array_equal(np.concatenate([r[0][name][k], r[1][name][k]]), get(), err_msg=name)
+    N = 2 * n_per
+    lw = inputs.resample_lw(N, 2.0, 0.2, seed=41)
+    st = inputs.state_bytes(N, 64, seed=42)
+    a0 = oracle.resample(lw, seed=7, epoch=0)["anc"]
+    a1 = oracle.resample(lw, seed=7, epoch=1)["anc"]
+    np.testing.assert_array_equal(np.concatenate([r[0]["resample"][0], r[1]["resample"][0]]), a1)
+    np.testing.assert_array_equal(np.concatenate([r[0]["resample"][1], r[1]["resample"][1]]), st[a0][a1])
