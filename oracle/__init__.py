@@ -283,9 +283,10 @@ class Smc:
         return out
 
     def stats(self):
-        out = np.zeros(6, dtype=np.uint64)
+        out = np.zeros(7, dtype=np.uint64)
         lib().oracle_smc_stats(self.h, _p(out, C.c_uint64))
-        keys = ["epochs", "resamples", "draws", "overflow", "alive_particle_steps", "status"]
+        keys = ["epochs", "resamples", "draws", "overflow", "alive_particle_steps", "status",
+                "guard"]
         return {k: int(v) for k, v in zip(keys, out)}
 
 

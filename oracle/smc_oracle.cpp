@@ -21,10 +21,13 @@
 //                    geometric E[Z] = 2; SSM vs Kalman (pinned)
 //   crbd             E[Z] vs the closed-form CRBD likelihood; prior-
 //                    integrated Z by quadrature                    (pinned)
-//   clads2           sigma=0, alpha=1 reduces to CRBD closed form  (pinned
-//                    for that special case; general case "parity unpinned")
-//   seir             tiny-population exact forward algorithm       (pinned
-//                    for fixed parameters; priors case "parity unpinned")
+//   clads2           sigma=0, alpha=1 reduces to CRBD closed form; sigma=0,
+//                    alpha!=1 vs the rate-level ladder of backward ODEs;
+//                    sigma>0 vs a forward simulation of a cherry; prior
+//                    block by KS tests                             (pinned)
+//   seir             tiny-population exact forward algorithm, fixed
+//                    parameters and with priors (QMC prior integral);
+//                    prior block by KS tests                       (pinned)
 //
 // Build: g++ -O2 -std=c++17 -ffp-contract=off -fPIC -shared (see build()).
 // =============================================================================
@@ -370,10 +373,14 @@ struct CrbdModel {
 // Rate guard: a lineage rate above kMaxRate (or not finite)
 // is outside the model's support; the particle's weight becomes -inf and the
 // block ends at once ("kill": branch index and pc advance, nothing else).
+// The threshold is params[5] (default 1e4); every kill is counted (stats
+// "guard") so runs can report how often the truncation acts.
 const double CLADS2_MAX_RATE = 1e4;
 struct Clads2Model {
   std::vector<Branch> br;
   double rho = 1.0, lam0_fixed = -1.0, sigma_fixed = -1.0, alpha_fixed = -1.0, eps_fixed = -1.0;
+  double max_rate = CLADS2_MAX_RATE;
+  mutable uint64_t* guard = nullptr;   // rate-guard kills (R-14b), owned by the Smc loop
   bool root_first_left = true;
   uint64_t stack_cap = 1024, event_cap = (1u << 22);
   static const int PEND = 6;
@@ -391,11 +398,11 @@ struct Clads2Model {
     f[5] = s.eps; f[6] = s.lam;
     for (int i = 0; i < PEND; ++i) f[7 + i] = i < s.sp ? s.pend[i] : 0.0;
   }
-  static bool bad_rate(double r) { return !(r <= CLADS2_MAX_RATE); }
+  bool bad_rate(double r) const { return !(r <= max_rate); }
   double daughter(const State& s, double lam, double z) const {
     return s.alpha * lam * std::exp(s.sigma * z);
   }
-  // 1 undetected, 0 detected or rate out of range, -1 stack/event overflow
+  // 1 undetected, 0 detected, -1 stack/event overflow, -2 rate out of range
   int undetected(double s0, double lam0, const State& st, Stream& rs) const {
     std::vector<std::pair<double, double>> stack;
     stack.push_back(std::make_pair(s0, lam0));
@@ -416,7 +423,7 @@ struct Clads2Model {
           double za = sample_normal(rs, 0.0, 1.0);
           double zb = sample_normal(rs, 0.0, 1.0);
           double la = daughter(st, lam, za), lb = daughter(st, lam, zb);
-          if (bad_rate(la) || bad_rate(lb)) return 0;
+          if (bad_rate(la) || bad_rate(lb)) return -2;
           if (stack.size() >= stack_cap) return -1;
           stack.push_back(std::make_pair(s, lb));
           lam = la;
@@ -428,6 +435,7 @@ struct Clads2Model {
     return 1;
   }
   int kill(State& s, double& lw) const {
+    if (guard) ++*guard;
     lw = -INFINITY;
     s.branch = s.branch + 1;
     s.pc = (s.branch == (int)br.size()) ? PC_STOP : 1;
@@ -468,8 +476,12 @@ struct Clads2Model {
       if (bad_rate(ls)) return kill(s, lw);
       int r = undetected(t, ls, s, rs);
       if (r != 1) {
-        if (r < 0) ++overflow;
-        return kill(s, lw);
+        if (r == -1) ++overflow;
+        if (r == -2) return kill(s, lw);            // rate guard inside the side tree
+        lw = -INFINITY;
+        s.branch = s.branch + 1;
+        s.pc = (s.branch == (int)br.size()) ? PC_STOP : 1;
+        return 1;
       }
       lw = lw + LN2;
       s.lam = daughter(s, s.lam, zc);
@@ -512,7 +524,7 @@ Block side_block(uint64_t seed, uint32_t id0, uint32_t id1, uint32_t n, uint32_t
   return philox4x32_10(id0, id1, n, (tag << 28) | t, (uint32_t)seed, (uint32_t)(seed >> 32));
 }
 
-enum { SIDE_UNDETECTED = 0, SIDE_DETECTED = 1, SIDE_OVERFLOW = 2 };
+enum { SIDE_UNDETECTED = 0, SIDE_DETECTED = 1, SIDE_OVERFLOW = 2, SIDE_GUARD = 3 };
 
 struct CrbdLRModel : CrbdModel {
   uint64_t seed = 0;
@@ -605,7 +617,7 @@ struct Clads2LRModel : Clads2Model {
         double th = TWO_PI * hq(Z.v[2], Z.v[3]);
         double za = r * std::cos(th), zb = r * std::sin(th);
         double la = daughter(st, v.lam, za), lb = daughter(st, v.lam, zb);
-        if (bad_rate(la) || bad_rate(lb)) return SIDE_DETECTED;   // rate guard: reject
+        if (bad_rate(la) || bad_rate(lb)) return SIDE_GUARD;      // rate guard: reject
         Block Cb = philox4x32_10(v.a, v.b, n, (TAG_CHILD << 28) | t, (uint32_t)seed, (uint32_t)(seed >> 32));
         stack.push_back(Node{Cb.v[0], Cb.v[1], s2, la});
         stack.push_back(Node{Cb.v[2], Cb.v[3], s2, lb});
@@ -654,6 +666,7 @@ struct Clads2LRModel : Clads2Model {
       int r = side_tree((uint32_t)k, roots[k].s, roots[k].lam, s, n, t, count);
       if (r != SIDE_UNDETECTED) {
         if (r == SIDE_OVERFLOW) ++overflow;
+        if (r == SIDE_GUARD && guard) ++*guard;
         dead = true;
       }
     }
@@ -971,7 +984,7 @@ struct SmcBase {
   double logz = 0.0;
   int status = E_OK;
   bool finished = false;
-  uint64_t draws = 0, overflow = 0, resamples = 0, alive_steps = 0;
+  uint64_t draws = 0, overflow = 0, resamples = 0, alive_steps = 0, guard = 0;
   uint32_t ess_a = 1, ess_b = 1;        // tau = a / b (>= 1: resample at every checkpoint)
   double last_ess = 0.0;
   bool carry = false;                   // last checkpoint did not resample: lw accumulates
@@ -985,6 +998,8 @@ struct SmcBase {
 inline void set_side_draws(...) {}
 inline void set_side_draws(CrbdLRModel& m, uint64_t* d) { m.draws = d; }
 inline void set_side_draws(Clads2LRModel& m, uint64_t* d) { m.draws = d; }
+inline void set_guard(...) {}
+inline void set_guard(Clads2Model& m, uint64_t* g) { m.guard = g; }
 
 // Adapter: the Alg. 1 loop calls step(); lineage-keyed models need (n, t).
 template <class M> struct StepCall {
@@ -1007,6 +1022,7 @@ struct Smc : SmcBase {
   Smc(const M& m, uint64_t n, uint64_t s) : model(m) {
     N = n; seed = s;
     set_side_draws(model, &draws);
+    set_guard(model, &guard);
     st.assign(N, typename M::State());
     lw.assign(N, 0.0);
     anc.resize(N);
@@ -1224,6 +1240,7 @@ void* oracle_smc_create(int kind, const double* data, uint64_t data_len,
       m.root_first_left = T.ntips(l) <= T.ntips(r);
       m.rho = P(0, 1.0); m.lam0_fixed = P(1, -1.0); m.sigma_fixed = P(2, -1.0);
       m.alpha_fixed = P(3, -1.0); m.eps_fixed = P(4, -1.0);
+      m.max_rate = P(5, CLADS2_MAX_RATE);
       return new Smc<Clads2Model>(m, N, seed);
     }
     case K_CRBD_LR: {
@@ -1246,6 +1263,7 @@ void* oracle_smc_create(int kind, const double* data, uint64_t data_len,
       m.root_first_left = T.ntips(l) <= T.ntips(r);
       m.rho = P(0, 1.0); m.lam0_fixed = P(1, -1.0); m.sigma_fixed = P(2, -1.0);
       m.alpha_fixed = P(3, -1.0); m.eps_fixed = P(4, -1.0);
+      m.max_rate = P(5, CLADS2_MAX_RATE);
       m.seed = seed;
       return new Smc<Clads2LRModel>(m, N, seed);
     }
@@ -1326,12 +1344,13 @@ void oracle_smc_anc(void* h, uint32_t* out) {
   SmcBase* s = (SmcBase*)h;
   std::memcpy(out, s->anc.data(), s->N * sizeof(uint32_t));
 }
-// stats: [epochs_done, resamples, draws, overflow, alive_particle_steps, status]
+// stats: [epochs_done, resamples, draws, overflow, alive_particle_steps, status,
+//         rate-guard kills (ClaDS2, R-14b)]
 void oracle_smc_stats(void* h, uint64_t* out) {
   SmcBase* s = (SmcBase*)h;
   out[0] = s->resamples + (s->finished ? 1 : 0);
   out[1] = s->resamples; out[2] = s->draws; out[3] = s->overflow;
-  out[4] = s->alive_steps; out[5] = (uint64_t)s->status;
+  out[4] = s->alive_steps; out[5] = (uint64_t)s->status; out[6] = s->guard;
 }
 void oracle_smc_destroy(void* h) { delete (SmcBase*)h; }
 

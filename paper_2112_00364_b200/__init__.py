@@ -58,7 +58,8 @@ class smc_stats_t(C.Structure):
                 ("draws", C.c_uint64), ("ms_propagate", C.c_double), ("ms_resample", C.c_double),
                 ("timed_epochs", C.c_uint64), ("side_roots", C.c_uint64),
                 ("max_rounds", C.c_uint32), ("max_side_nodes", C.c_uint32),
-                ("distinct", C.c_uint64), ("ms_kernel", C.c_double * 4)]
+                ("distinct", C.c_uint64), ("ms_kernel", C.c_double * 4),
+                ("guard_kills", C.c_uint64)]
 
 
 ALLGATHER_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)

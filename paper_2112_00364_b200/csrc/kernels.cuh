@@ -67,6 +67,7 @@ struct Ctrl {
   unsigned max_side_nodes;           // diag: largest per-particle side-tree node count
   unsigned holes;                    // in-place resampling (R-21): slots without offspring
   unsigned bar_count, bar_gen;       // grid barrier of resample_fused_kernel
+  unsigned long long guard_kills;    // ClaDS2 rate guard (R-14b): killed particle-steps
 };
 
 enum { ST_OK = 0, ST_REJECTED = 4, ST_NAN = 5, ST_OVERFLOW = 6 };
@@ -385,6 +386,7 @@ __global__ void __launch_bounds__(kThreads, M::kMinBlocks) propagate_kernel(Prop
     if (o) atomicAdd(&a.ctrl->overflow, o);
     if (dr) atomicAdd(&a.ctrl->draws, dr);
   }
+  if (dg.guard) atomicAdd(&a.ctrl->guard_kills, dg.guard);   // rare (ClaDS2 only)
 }
 
 // anc[i] = base + i (identity before the first resample)

@@ -75,7 +75,7 @@ struct NodeOut {
   double s2, la, lb;             // daughters' start age and rates (rates: ClaDS2)
   unsigned long long ida, idb;   // daughters' ids
 };
-enum { NODE_LEAF = 0, NODE_DETECTED = 1, NODE_BIRTH = 2 };
+enum { NODE_LEAF = 0, NODE_DETECTED = 1, NODE_BIRTH = 2, NODE_GUARD = 3 };
 
 // Per-owner constants kept in shared memory during phase 2.
 struct OwnerCrbd { double tot, pb; };
@@ -236,7 +236,7 @@ struct Clads2LR {
     const double za = rad * cos(th), zb = rad * sin(th);
     out.la = ow.alpha * lam * exp(ow.sigma * za);
     out.lb = ow.alpha * lam * exp(ow.sigma * zb);
-    if (Clads2::bad_rate(out.la) || Clads2::bad_rate(out.lb)) return NODE_DETECTED;   // rate guard
+    if (Clads2::bad_rate(out.la) || Clads2::bad_rate(out.lb)) return NODE_GUARD;   // rate guard
     const uint4 Cb = side_block(seed, id, n, t, kTagChild);
     out.s2 = s - d;
     out.ida = ((unsigned long long)Cb.y << 32) | Cb.x;
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
   // neighbouring s_ovtop, which thread 0 writes after (A) (racecheck)
   __shared__ __align__(16) int s_wsum[kLRThreads / 32];
   __shared__ unsigned s_batch;
-  __shared__ int s_dead[kOwners];             // 0 alive, 1 detected/rejected, 2 node cap
+  __shared__ int s_dead[kOwners];             // 0 alive, 1 detected, 2 node cap, 3 rate guard
   __shared__ unsigned s_nodes[kOwners];
   __shared__ typename M::Owner s_own[kOwners];
   __shared__ int s_taskcap;
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
   };
 
   long long key = LLONG_MIN;
-  unsigned long long n_end = 0, n_start = 0, drw = 0, ovf = 0, roots = 0;
+  unsigned long long n_end = 0, n_start = 0, drw = 0, ovf = 0, roots = 0, guard = 0;
   bool bad = false;
   unsigned max_rounds = 0, max_nodes = 0;
   const int warp_id = tid >> 5, lane_id = tid & 31;
@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
           Rng r(seed, (uint32_t)(p.shard_base + i), epoch);
           int k = 0;
           auto push = [&](double s0, double lam0, unsigned kk) { push_task(o, s0, lam0, root_id(kk)); };
-          if (!M::main_part(st, lw[q], r, C, s_own[o], k, push)) s_dead[o] = 1;
+          if (!M::main_part(st, lw[q], r, C, s_own[o], k, push)) s_dead[o] = 3;   // rate guard
           K[q] = k;
           roots += (unsigned long long)k;
           drw += 2ull * r.blk - (r.has_spare ? 1ull : 0ull);
@@ -457,8 +457,8 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
         drw += 2;
         NodeOut out;
         const int res = M::node(ts, tl, tidv, s_own[o], n_owner, epoch, seed, rho, out);
-        if (res == NODE_DETECTED) {
-          atomicCAS(&s_dead[o], 0, 1);
+        if (res == NODE_DETECTED || res == NODE_GUARD) {
+          atomicCAS(&s_dead[o], 0, res == NODE_GUARD ? 3 : 1);
         } else if (res == NODE_BIRTH) {
           push_pair(o, out.s2, out.lb, out.idb, out.la, out.ida);   // first daughter on top
         }
@@ -482,6 +482,7 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
           const int dead = s_dead[o];
           if (dead) {
             w = -INFINITY;
+            if (dead == 3) ++guard;
             if (dead == 2) {
               ++ovf;
               atomicMin(&p.ctrl->first_err, (unsigned long long)(p.shard_base + i));
@@ -541,6 +542,7 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
     if (dr) atomicAdd(&p.ctrl->draws, dr);
   }
   if (any_ovf && lane == 0 && ovf) atomicAdd(&p.ctrl->overflow, ovf);
+  if (guard) atomicAdd(&p.ctrl->guard_kills, guard);   // rare (ClaDS2 only)
   // diagnostics (one atomic per warp)
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {

@@ -30,7 +30,8 @@ struct ModelConst {
 // Per-thread diagnostics sink.
 struct Diag {
   unsigned long long overflow;
-  __device__ Diag() : overflow(0) {}
+  unsigned guard;                // ClaDS2 rate-guard kills (R-14b)
+  __device__ Diag() : overflow(0), guard(0) {}
 };
 
 __device__ __forceinline__ uint4 ldp(const uint4* planes, unsigned long long stride, int p,
@@ -259,7 +260,7 @@ struct Clads2 {
           const double za = d_normal(r, 0.0, 1.0);
           const double zb = d_normal(r, 0.0, 1.0);
           const double la = daughter(st, lam, za), lb = daughter(st, lam, zb);
-          if (bad_rate(la) || bad_rate(lb)) return 0;
+          if (bad_rate(la) || bad_rate(lb)) return -2;
           if (sp >= kStackCap) return -1;
           stk_s[sp] = s; stk_l[sp] = lb; ++sp;
           lam = la;
@@ -292,7 +293,7 @@ struct Clads2 {
     const double tp = __ldg(b), tc = __ldg(b + 1);
     const bool internal = __ldg(b + 2) != 0.0;
     const bool first_left = __ldg(b + 3) != 0.0;
-    bool killed = bad_rate(s.lam);
+    bool killed = bad_rate(s.lam), detected = false;
     double t = tp;
     while (!killed) {
       const double dt = d_exp(r, s.lam);
@@ -308,7 +309,8 @@ struct Clads2 {
       if (bad_rate(ls)) { killed = true; break; }
       const int u = undetected(t, ls, s, rho, r);
       if (u != 1) {
-        if (u < 0) ++dg.overflow;
+        if (u == -1) ++dg.overflow;
+        if (u != -2) detected = true;   // detected / overflow: not a guard kill
         killed = true;
         break;
       }
@@ -331,7 +333,10 @@ struct Clads2 {
       lw = lw + log(rho);
       if (s.branch + 1 < C.n) s.lam = pop(s);
     }
-    if (killed) lw = -INFINITY;
+    if (killed) {
+      lw = -INFINITY;
+      if (!detected) ++dg.guard;
+    }
     s.branch = s.branch + 1;
     s.pc = (s.branch == C.n) ? kStop : 1;
     return true;

@@ -178,3 +178,208 @@ def seir_exact_log_z(y, prm, nh, sm0, eh0=0, im0=0):
                     new[(a, b, c, d) + mk] += w * pm_
         dist = new
     return math.log(sum(dist.values()))
+
+
+def seir_exact_z_batch(y, prm, nh, sm0, eh0=0, im0=0):
+    """Exact Z(theta) of the tiny-population SEIR model for a BATCH of parameter
+    vectors: prm = (lam_h, del_h, gam_h, lam_m, del_m, rho), each an array of
+    shape (M,).  Same forward algorithm as ``seir_exact_log_z`` (state space
+    enumerated per day, binomial pmfs from their definition); the state
+    enumeration does not depend on theta (the infection probabilities
+    1 - exp(-i/n_h) and the mosquito birth / survival rates are constants), so
+    every probability is carried as an (M,) array.  Returns Z (not log Z)."""
+    lam_h, del_h, gam_h, lam_m, del_m, rho = (np.asarray(v, dtype=np.float64) for v in prm)
+    M = lam_h.shape[0]
+    nu_m, mu_m = 1.0 / 7.0, 6.0 / 7.0
+
+    def bpmf(k, n, p):                      # p: scalar or (M,) array
+        return math.comb(n, k) * np.power(p, k) * np.power(1.0 - p, n - k)
+
+    def cpmf(n, p):                         # constant-p pmf vector (length n+1)
+        return np.array([math.comb(n, k) * p ** k * (1 - p) ** (n - k) for k in range(n + 1)])
+
+    hmemo, mmemo = {}, {}
+
+    def human(sh, eh, ih, rh, im):
+        key = (sh, eh, ih, rh, im)
+        if key in hmemo:
+            return hmemo[key]
+        out = defaultdict(lambda: np.zeros(M))
+        ph = 1.0 - math.exp(-im / nh)
+        for tau_h in range(sh + 1):
+            p1 = math.comb(sh, tau_h) * ph ** tau_h * (1 - ph) ** (sh - tau_h)
+            if p1 == 0.0:
+                continue
+            for de_h in range(tau_h + 1):
+                p2 = p1 * bpmf(de_h, tau_h, lam_h)
+                for di_h in range(eh + 1):
+                    p3 = p2 * bpmf(di_h, eh, del_h)
+                    for dr_h in range(ih + 1):
+                        k2 = (sh - de_h, eh + de_h - di_h, ih + di_h - dr_h, rh + dr_h, di_h)
+                        out[k2] = out[k2] + p3 * bpmf(dr_h, ih, gam_h)
+        hmemo[key] = out
+        return out
+
+    def mosquito(sm, em, im, ih):
+        key = (sm, em, im, ih)
+        if key in mmemo:
+            return mmemo[key]
+        pm = 1.0 - math.exp(-ih / nh)
+        births = cpmf(sm + em + im, nu_m)
+        out = defaultdict(lambda: np.zeros(M))
+        for tau_m in range(sm + 1):
+            q1 = math.comb(sm, tau_m) * pm ** tau_m * (1 - pm) ** (sm - tau_m)
+            if q1 == 0.0:
+                continue
+            for de_m in range(tau_m + 1):
+                q2 = q1 * bpmf(de_m, tau_m, lam_m)
+                for di_m in range(em + 1):
+                    w = q2 * bpmf(di_m, em, del_m)
+                    ps = np.convolve(cpmf(sm - de_m, mu_m), births)
+                    pe = cpmf(em + de_m - di_m, mu_m)
+                    pi = cpmf(im + di_m, mu_m)
+                    for a, pa in enumerate(ps):
+                        for b, pb in enumerate(pe):
+                            for c, pc in enumerate(pi):
+                                cst = pa * pb * pc
+                                if cst != 0.0:
+                                    out[(a, b, c)] = out[(a, b, c)] + w * cst
+        mmemo[key] = out
+        return out
+
+    dist = {(nh - 1 - eh0, eh0, 1, 0, sm0, 0, im0): np.ones(M)}
+    for yt in y:
+        new = defaultdict(lambda: np.zeros(M))
+        for (sh, eh, ih, rh, sm, em, im), pr in dist.items():
+            H = human(sh, eh, ih, rh, im)
+            Mq = mosquito(sm, em, im, ih)
+            for (a, b, c, d, z), ph in H.items():
+                if yt > z:
+                    continue
+                w = pr * ph * bpmf(yt, z, rho)
+                for mk, pm_ in Mq.items():
+                    k2 = (a, b, c, d) + mk
+                    new[k2] = new[k2] + w * pm_
+        dist = new
+    return sum(dist.values())
+
+
+# --------------------------------------------------------------------------
+# ClaDS2 (DESIGN.md R-14) with sigma = 0: rates are deterministic given the
+# number of speciation events k a lineage descends through, lambda_k =
+# alpha^k lambda0, mu_k = eps lambda_k.  The backward equations of the
+# birth-death process (the CRBD E/D pair of SURVEY §8(c), with the daughters'
+# rates one level up) then form a ladder:
+#   dE_k/dt = mu_k - (lam_k + mu_k) E_k + lam_k E_{k+1}^2,     E_k(0) = 1 - rho
+#   dD_k/dt = -(lam_k + mu_k) D_k + 2 lam_k E_{k+1} D_{k+1},   D_k(0) = rho (tips)
+#   internal node c at age t_c:  D_{c,k} = lam_k D_{l,k+1} D_{r,k+1}
+#   root (the INIT rate is level 0; its daughters are level 1):
+#   L = D_{l,1} D_{r,1}
+# Truncated at level K (level K keeps rate lam_K: a CRBD lineage).
+def _clads2_rates(lam0, alpha, eps, K):
+    lam = lam0 * alpha ** np.arange(K + 1, dtype=np.float64)
+    return lam, eps * lam
+
+
+def clads2_ladder_E(t, lam0, alpha, eps, rho, K=60):
+    """E_k(t), k = 0..K (probability that a level-k lineage alive at age t
+    leaves no sampled descendant)."""
+    from scipy.integrate import solve_ivp
+    lam, mu = _clads2_rates(lam0, alpha, eps, K)
+
+    def f(_, E):
+        up = np.append(E[1:], E[-1])
+        return mu - (lam + mu) * E + lam * up * up
+
+    if t == 0.0:
+        return np.full(K + 1, 1.0 - rho)
+    sol = solve_ivp(f, (0.0, t), np.full(K + 1, 1.0 - rho), rtol=1e-11, atol=1e-13, method="DOP853")
+    return sol.y[:, -1]
+
+
+def clads2_ladder_log_lik(tree, lam0, alpha, eps, rho=1.0, K=60):
+    """log L of the fixed tree under ClaDS2 with sigma = 0 (see above)."""
+    from scipy.integrate import solve_ivp
+    lam, mu = _clads2_rates(lam0, alpha, eps, K)
+    par, left, right, age = tree["parent"], tree["left"], tree["right"], tree["age"]
+    root = tree["root"]
+
+    def branch(c, Dc):
+        """Integrate (E, D) from the child's age to the parent's age; D is kept
+        normalised (returned with its log scale)."""
+        tc, tp = age[c], age[par[c]]
+        E0 = clads2_ladder_E(tc, lam0, alpha, eps, rho, K)
+
+        def f(_, y):
+            E, D = y[:K + 1], y[K + 1:]
+            Eu = np.append(E[1:], E[-1])
+            Du = np.append(D[1:], D[-1])
+            return np.concatenate([mu - (lam + mu) * E + lam * Eu * Eu,
+                                   -(lam + mu) * D + 2.0 * lam * Eu * Du])
+
+        sol = solve_ivp(f, (tc, tp), np.concatenate([E0, Dc]), rtol=1e-11, atol=1e-15,
+                        method="DOP853")
+        return sol.y[K + 1:, -1]
+
+    def subtree(c):
+        """(D_{c,k} at the child's age, normalised; log scale)."""
+        if left[c] < 0:
+            return np.full(K + 1, rho), 0.0
+        Dl, sl = top(left[c])
+        Dr, sr = top(right[c])
+        Dlu, Dru = np.append(Dl[1:], Dl[-1]), np.append(Dr[1:], Dr[-1])
+        D = lam * Dlu * Dru
+        m = D.max()
+        return D / m, sl + sr + math.log(m)
+
+    def top(c):
+        D, s = subtree(c)
+        Dt = branch(c, D)
+        m = Dt.max()
+        return Dt / m, s + math.log(m)
+
+    Dl, sl = top(left[root])
+    Dr, sr = top(right[root])
+    return math.log(Dl[1] * Dr[1]) + sl + sr
+
+
+def clads2_cherry_forward(T, lam0, alpha, sigma, eps, rho, n, seed):
+    """Brute-force FORWARD simulation of the generative ClaDS2 model (not the
+    SMC's backward construction): a cherry (two tips, root age T) has
+    likelihood L = P(a root daughter leaves exactly one sampled extant
+    descendant)^2 with the two root daughters independent (rates
+    alpha lam0 e^{sigma z}).  Each daughter lineage is simulated forward to
+    the present: next event after Exp(lam (1 + eps)); at the present the
+    lineage is sampled with probability rho; an event is a birth with
+    probability 1/(1 + eps) (two daughters with rates alpha lam e^{sigma z})
+    and a death otherwise.  Returns (estimate of L, its standard error) from
+    two independent halves (mean(X) * mean(Y) is unbiased for p^2)."""
+    g = np.random.Generator(np.random.PCG64(seed))
+
+    def one():
+        count = 0
+        stack = [(T, alpha * lam0 * math.exp(sigma * g.standard_normal()))]
+        while stack:
+            s, lam = stack.pop()
+            while True:
+                d = g.exponential(1.0 / (lam * (1.0 + eps)))
+                if d > s:
+                    if g.random() < rho:
+                        count += 1
+                        if count > 1:
+                            return 0
+                    break
+                s -= d
+                if g.random() < 1.0 / (1.0 + eps):
+                    za, zb = g.standard_normal(2)
+                    stack.append((s, alpha * lam * math.exp(sigma * zb)))
+                    lam = alpha * lam * math.exp(sigma * za)
+                    continue
+                break
+        return 1 if count == 1 else 0
+
+    x = np.array([one() for _ in range(n)], dtype=np.float64)
+    y = np.array([one() for _ in range(n)], dtype=np.float64)
+    px, py = x.mean(), y.mean()
+    se = math.sqrt(py * py * x.var(ddof=1) / n + px * px * y.var(ddof=1) / n)
+    return px * py, se
