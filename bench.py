@@ -170,16 +170,17 @@ def oracle_sweep_rate(wl, budget_s=15.0, n_cap=None):
     else:
         data, params = inputs.seir_series(), None
     n = 1000
-    t0 = time.perf_counter()
     ea, eb = (int(x) for x in getattr(oracle_sweep_rate, "ess", "1/1").split("/"))
-    s = oracle.Smc(kind, data, params, n, 12345)
-    s.set_ess(ea, eb)
-    s.set_inplace(getattr(oracle_sweep_rate, "inplace", False))
-    s.run()
-    dt = time.perf_counter() - t0
-    n = max(1000, int(n * budget_s / max(dt, 1e-3)))
+    if budget_s > 0:
+        t0 = time.perf_counter()
+        s = oracle.Smc(kind, data, params, n, 12345)
+        s.set_ess(ea, eb)
+        s.set_inplace(getattr(oracle_sweep_rate, "inplace", False))
+        s.run()
+        dt = time.perf_counter() - t0
+        n = max(1000, int(n * budget_s / max(dt, 1e-3)))
     if n_cap:
-        n = min(n, n_cap)
+        n = min(n, n_cap) if budget_s > 0 else n_cap
     t0 = time.perf_counter()
     s = oracle.Smc(kind, data, params, n, 12345)
     s.set_ess(ea, eb)
@@ -188,6 +189,15 @@ def oracle_sweep_rate(wl, budget_s=15.0, n_cap=None):
     dt = time.perf_counter() - t0
     st = s.stats()
     return st["alive_particle_steps"] / dt, f"one full sweep, N={n} particles, seed 12345", dt, st
+
+
+def oracle_draws_per_step(wl, n=20000, seed=12345):
+    """Algorithmic propagation work: uniforms drawn per
+    particle-step as counted by the oracle (one full sweep of n particles; the
+    GPU's own counter also holds speculative side-tree nodes of the cooperative
+    kernel, so the roofline uses this schedule-independent count)."""
+    _, sample, _, st = oracle_sweep_rate(wl, n_cap=n, budget_s=0.0)
+    return st["draws"] / max(st["alive_particle_steps"], 1), sample
 
 
 def oracle_resample_rate(n_full, budget_s=10.0):
@@ -260,6 +270,7 @@ def bench_sweeps(args, wl, smc, torch, world, rank):
           for _ in range(args.steps)]
     steps_done = 0
     draws = 0
+    guard = 0
     alive_steps = 0
     logzs = []
     barrier(torch, world)
@@ -273,6 +284,7 @@ def bench_sweeps(args, wl, smc, torch, world, rank):
             ev[k][1].record(stream)
             st = h.stats()
             draws += st["draws"]
+            guard += st["guard_kills"]
             alive_steps += st["alive_particle_steps"]
             steps_done += st["epochs"]
             logzs.append(h.log_z)
@@ -312,7 +324,7 @@ def bench_sweeps(args, wl, smc, torch, world, rank):
     launches = args.steps * (2 * per_epoch + 1) * ((E + 1) // 2)
     return dict(h=h, model=model, N=N, t_ms=t_ms, value=value, sweeps=sweeps_per_s, prop_ms=prop_ms,
                 res_bytes=res_bytes, resamples_per_sweep=n_resamples / args.steps,
-                res_ms=res_ms, draws=draws, alive_steps=alive_steps, epochs=steps_done,
+                res_ms=res_ms, draws=draws, guard=guard, alive_steps=alive_steps, epochs=steps_done,
                 launches=launches, fused=fused, clocks=clk.summary(torch.cuda.current_device()),
                 logz=float(np.mean(logzs)))
 
@@ -426,6 +438,60 @@ def bench_resample(args, wl, smc, torch):
                 clocks=clk.summary(torch.cuda.current_device()))
 
 
+def resample_line(args, smc, torch, world, rank, pk, pk_kind, n, sigma, inplace=False, steps=None,
+                  warmup=None):
+    """configs[4] on one GPU: one resampling step of n particles x 64 B."""
+    hbm_peak = pk["hbm_gbs"]
+    sub_args = argparse.Namespace(**vars(args))
+    sub_args.n, sub_args.sigma, sub_args.inplace = n, sigma, inplace
+    sub_args.steps = steps or max(3, min(args.steps, 10))
+    sub_args.warmup = warmup or max(3, args.warmup)
+    args = sub_args
+    r = bench_resample(args, WORKLOADS["resample"], smc, torch)
+    achieved = r["alg_bytes"] / (r["t_ms"] * 1e-3) / 1e9
+    n, D = r["n"], r["D"]
+    g_bytes = n * 12 + 64 * (D + n)          # anc_gather: lw read, anc write, states
+    kname = "anc_gather_kernel (ancestors + fused gather)"
+    fused = r["fused"]
+    if fused:                                # N fits the co-resident grid: one launch
+        kname = "resample_fused_kernel (quantise + exact sum, grid barrier, ancestors + gather, log Z)"
+    metric = "resample effective HBM GB/s (B_alg = N*20 + 64*(D+N))"
+    if args.inplace:
+        # offspring: lw 8 + O_k 4; permute: O_k 4 + survivors' anc 4 D + hole/extra
+        # lists 8 H; fill: lists 8 H + anc 4 H + state 2*64 H   (H = N - D holes)
+        H = n - D
+        g_bytes = n * 16 + 4 * D + H * (20 + 2 * 64)
+        kname = "in-place chain (offspring + permute + fill_holes kernels, R-21)"
+        metric = ("resample effective GB/s, in place (B_alg of the out-of-place step, "
+                  "N*20 + 64*(D+N), per unit time)")
+    g_ms = r["ms_kernel"][2]
+    g_ach = g_bytes / (g_ms * 1e-3) / 1e9
+    tr = None if args.inplace else traffic(f"resample:{n}:anc_gather")
+    line = dict(metric=metric, value=achieved,
+                unit="GB/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
+                ms_per_step=r["t_ms"], higher_is_better=True, scaling="weak", vs_baseline=None,
+                dtype="f64/u128", data="synthetic",
+                config=dict(workload="resample", desc=WORKLOADS["resample"]["desc"], n_per_gpu=r["n"],
+                            state_bytes=64, sigma=args.sigma, l2="flushed between steps",
+                            inplace=args.inplace),
+                roofline=dict(bound="hbm", kernel=kname,
+                              achieved=g_ach, peak=hbm_peak, unit="GB/s", frac=g_ach / hbm_peak,
+                              traffic=(tr["bytes"] if tr else None),
+                              algorithmic_bytes=g_bytes, ms=g_ms, peak_source=pk_kind),
+                chain_roofline=dict(bound="hbm", achieved=achieved, peak=hbm_peak, unit="GB/s",
+                                    frac=achieved / hbm_peak, algorithmic_bytes=r["alg_bytes"],
+                                    note=("max + resample_fused" if fused else
+                                          "max + reduce + anc_gather + finalize") +
+                                         "; B_alg excludes the standalone max pass (8 B/particle)"),
+                kernel_ms=(dict(max=r["ms_kernel"][0], resample_fused=r["ms_kernel"][2]) if fused else
+                           dict(zip(["max", "reduce", "inplace_chain" if args.inplace else "anc_gather",
+                                     "finalize"], r["ms_kernel"]))),
+                distinct_ancestors=D,
+                gpu_launches=(7 if args.inplace else 3 if fused else 5) * args.steps, clocks=r["clocks"])
+    del r
+    return line
+
+
 def barrier(torch, world):
     if world > 1:
         import torch.distributed as dist
@@ -480,74 +546,87 @@ def run_ours(args, wl):
             print(json.dumps(line), flush=True)
         return
     if wl["model"] == "resample":
-        r = bench_resample(args, wl, smc, torch)
-        achieved = r["alg_bytes"] / (r["t_ms"] * 1e-3) / 1e9
-        n, D = r["n"], r["D"]
-        g_bytes = n * 12 + 64 * (D + n)          # anc_gather: lw read, anc write, states
-        kname = "anc_gather_kernel (ancestors + fused gather)"
-        fused = r["fused"]
-        if fused:                                # N fits the co-resident grid: one launch
-            kname = "resample_fused_kernel (quantise + exact sum, grid barrier, ancestors + gather, log Z)"
-        metric = "resample effective HBM GB/s (B_alg = N*20 + 64*(D+N))"
-        if args.inplace:
-            # offspring: lw 8 + O_k 4; permute: O_k 4 + survivors' anc 4 D + hole/extra
-            # lists 8 H; fill: lists 8 H + anc 4 H + state 2*64 H   (H = N - D holes)
-            H = n - D
-            g_bytes = n * 16 + 4 * D + H * (20 + 2 * 64)
-            kname = "in-place chain (offspring + permute + fill_holes kernels, R-21)"
-            metric = ("resample effective GB/s, in place (B_alg of the out-of-place step, "
-                      "N*20 + 64*(D+N), per unit time)")
-        g_ms = r["ms_kernel"][2]
-        g_ach = g_bytes / (g_ms * 1e-3) / 1e9
-        tr = None if args.inplace else traffic(f"resample:{n}:anc_gather")
-        line = dict(metric=metric, value=achieved,
-                    unit="GB/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
-                    ms_per_step=r["t_ms"], higher_is_better=True, scaling="weak", vs_baseline=None,
-                    dtype="f64/u128", data="synthetic",
-                    config=dict(workload="resample", desc=wl["desc"], n_per_gpu=r["n"],
-                                state_bytes=64, sigma=args.sigma, l2="flushed between steps",
-                                inplace=args.inplace),
-                    roofline=dict(bound="hbm", kernel=kname,
-                                  achieved=g_ach, peak=hbm_peak, unit="GB/s", frac=g_ach / hbm_peak,
-                                  traffic=(tr["bytes"] if tr else None),
-                                  algorithmic_bytes=g_bytes, ms=g_ms, peak_source=pk_kind),
-                    chain_roofline=dict(bound="hbm", achieved=achieved, peak=hbm_peak, unit="GB/s",
-                                        frac=achieved / hbm_peak, algorithmic_bytes=r["alg_bytes"],
-                                        note=("max + resample_fused" if fused else
-                                              "max + reduce + anc_gather + finalize") +
-                                             "; B_alg excludes the standalone max pass (8 B/particle)"),
-                    kernel_ms=(dict(max=r["ms_kernel"][0], resample_fused=r["ms_kernel"][2]) if fused else
-                               dict(zip(["max", "reduce", "inplace_chain" if args.inplace else "anc_gather",
-                                         "finalize"], r["ms_kernel"]))),
-                    distinct_ancestors=D,
-                    gpu_launches=(7 if args.inplace else 3 if fused else 5) * args.steps, clocks=r["clocks"])
+        line = resample_line(args, smc, torch, world, rank, pk, pk_kind, n=args.n or wl["n"],
+                             sigma=args.sigma, inplace=args.inplace, steps=args.steps,
+                             warmup=args.warmup)
         if rank == 0:
             print(json.dumps(line), flush=True)
         return
-    r = bench_sweeps(args, wl, smc, torch, world, rank)
+    draw_peak = smc.draw_peak() / 1e9
+    line = sweep_line(args, args.workload, wl, smc, torch, world, rank, pk, pk_kind, draw_peak,
+                      with_e2e=not args.no_e2e, with_cpu=not args.no_cpu_baseline)
+    if world == 1 and args.workload == "crbd" and not args.only:
+        # the other BASELINE configs, measured in the same run (the headline
+        # fields above stay configs[1]'s): configs[2] ClaDS2, configs[3] SEIR,
+        # configs[4] the resampling step at 2^26 and 2^28 particles
+        subs = {}
+        for key, name in (("c2_clads2", "clads2"), ("c3_seir", "seir")):
+            sl = sweep_line(args, name, WORKLOADS[name], smc, torch, world, rank, pk, pk_kind,
+                            draw_peak, with_e2e=False, with_cpu=False)
+            subs[key] = {k: sl[k] for k in ("metric", "value", "unit", "ms_per_step", "sweeps_per_s",
+                                            "mean_log_z", "phase_ms", "draws_per_particle_step",
+                                            "roofline", "resample_roofline", "clocks", "config",
+                                            "guard_kills_per_particle_step", "gpu_launches") if k in sl}
+        for lg in (26, 28):
+            rl = resample_line(args, smc, torch, world, rank, pk, pk_kind, n=1 << lg, sigma=1.0)
+            subs[f"c4_resample_2p{lg}"] = {k: rl[k] for k in ("metric", "value", "unit", "ms_per_step",
+                                                              "roofline", "chain_roofline", "kernel_ms",
+                                                              "distinct_ancestors", "clocks", "config")}
+        line["configs"] = subs
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def sweep_line(args, name, wl, smc, torch, world, rank, pk, pk_kind, draw_peak, with_e2e, with_cpu):
+    """One sweep workload (configs[1]-[3]): the JSON fields of its line."""
+    hbm_peak = pk["hbm_gbs"]
+    rng = args.rng if wl["model"] in ("crbd", "clads2") else "sequential"
+    ess = args.ess if name == args.workload else wl.get("ess", "1/1")
+    sub_args = argparse.Namespace(**vars(args))
+    sub_args.ess = ess
+    if name != args.workload:
+        sub_args.n = 0
+        sub_args.steps = max(3, min(args.steps, 5))
+        sub_args.warmup = max(3, args.warmup)
+        sub_args.inplace = False
+    oracle_sweep_rate.ess = ess
+    r = bench_sweeps(sub_args, wl, smc, torch, world, rank)
+    steps = sub_args.steps
     N = r["N"]
-    # propagation roofline: uniforms drawn per second against the
-    # issue-rate ceiling 148 SM x 128 lanes x f_max / 34 instructions per uniform
+    # propagation roofline (DESIGN.md §7): algorithmic uniforms per particle-step
+    # counted by the oracle on a sample of the same workload, times the GPU's
+    # particle-steps, per second of propagation, against the measured draw-rate
+    # ceiling (smc_draw_peak: divergence-free Philox + hq + fp64 Exp)
     f_max = float(pk.get("sm_max_mhz", 1965.0)) * 1e6
-    draw_peak = 148 * 128 * f_max / 34.0 / 1e9
-    draw_rate = r["draws"] / args.steps / max(r["prop_ms"] / args.steps * 1e-3, 1e-12) / 1e9
-    # dominant kernel: propagation (ALU); resample chain: HBM
+    derived_peak = 148 * 128 * f_max / 34.0 / 1e9
+    prop_s = max(r["prop_ms"] / steps * 1e-3, 1e-12)
+    gpu_rate = r["draws"] / steps / prop_s / 1e9
+    lin = rng == "lineage" and not wl.get("analytic")
+    try:
+        odps, osample = oracle_draws_per_step(wl, n=20000 if wl["model"] != "seir" else 5000)
+    except Exception as e:  # noqa: BLE001  (the oracle is a reported baseline, not the product)
+        odps, osample = None, f"oracle unavailable: {e}"
+    alg_rate = (odps * r["alive_steps"] / steps / prop_s / 1e9) if odps else None
+    peak = draw_peak if draw_peak else derived_peak
     prop_frac = r["prop_ms"] / max(r["prop_ms"] + r["res_ms"], 1e-9)
+    kname = ("propagate_lr_kernel" if lin else "propagate_kernel") + f"<{name}>"
     line = dict(metric="particle-steps/s", value=r["value"], unit="particle-steps/s",
-                n_gpus=world, steps=args.steps, warmup=args.warmup,
-                ms_per_step=r["t_ms"] / args.steps, higher_is_better=True, scaling="weak",
+                n_gpus=world, steps=steps, warmup=sub_args.warmup,
+                ms_per_step=r["t_ms"] / steps, higher_is_better=True, scaling="weak",
                 vs_baseline=None, dtype="f64", data="synthetic",
-                config=dict(workload=args.workload, desc=wl["desc"], n_per_gpu=N,
-                            rng=("analytic (no side trees)" if wl.get("analytic") else
-                                 args.rng if wl["model"] in ("crbd", "clads2") else "sequential"),
-                            ess_threshold=args.ess, inplace=args.inplace,
-                            epochs_per_sweep=r["epochs"] // args.steps,
+                config=dict(workload=name, desc=wl["desc"], n_per_gpu=N,
+                            rng=("analytic (no side trees)" if wl.get("analytic") else rng),
+                            ess_threshold=ess, inplace=sub_args.inplace,
+                            epochs_per_sweep=r["epochs"] // steps,
                             l2="flushed between steps (state fits L2 within a sweep)"),
                 sweeps_per_s=r["sweeps"], mean_log_z=r["logz"],
                 resamples_per_sweep=r["resamples_per_sweep"],
-                phase_ms=dict(propagate=r["prop_ms"] / args.steps, resample=r["res_ms"] / args.steps,
+                phase_ms=dict(propagate=r["prop_ms"] / steps, resample=r["res_ms"] / steps,
                               propagate_share=prop_frac),
-                draws_per_particle_step=r["draws"] / max(r["alive_steps"], 1),
+                draws_per_particle_step=dict(oracle=odps, oracle_sample=osample,
+                                             gpu=r["draws"] / max(r["alive_steps"], 1),
+                                             note="gpu counts speculative side-tree nodes (R-18)"
+                                             if lin else "identical streams"),
                 resample_roofline=dict(bound="hbm", achieved=r["res_bytes"] / (r["res_ms"] * 1e-3) / 1e9,
                                        peak=hbm_peak, unit="GB/s",
                                        frac=r["res_bytes"] / (r["res_ms"] * 1e-3) / 1e9 / hbm_peak,
@@ -555,29 +634,44 @@ def run_ours(args, wl):
                                                if r["fused"] else "reduce + anc_gather + finalize"),
                                        note="per epoch at this N (latency-bound at 10^6; "
                                             "see workload 'resample' for the HBM-bound sizes)"),
-                roofline=dict(bound="alu",
-                              kernel=("propagate_lr_kernel" if args.rng == "lineage" and wl["model"] in ("crbd", "clads2")
-                                      and not wl.get("analytic") else "propagate_kernel") + f"<{args.workload}>",
-                              achieved=draw_rate, peak=draw_peak, unit="Gdraws/s",
-                              frac=draw_rate / draw_peak,
-                              traffic=((traffic(f"{wl['model']}:{N}:propagate_lr_kernel") or {}).get("bytes")
-                                       if args.rng == "lineage" and not wl.get("analytic") else None),
-                              peak_source=f"derived: 148 SM x 128 lanes x {f_max/1e6:.0f} MHz / 34 instr per uniform (DESIGN.md s7)"),
+                roofline=dict(bound="alu", kernel=kname,
+                              achieved=alg_rate if alg_rate else gpu_rate, peak=peak, unit="Gdraws/s",
+                              frac=(alg_rate if alg_rate else gpu_rate) / peak,
+                              achieved_gpu_count=gpu_rate,
+                              traffic=((traffic(f"{wl['model']}:{N}:{kname.split('<')[0]}") or {}).get("bytes")),
+                              peak_source=("measured live: smc_draw_peak (Philox + hq + fp64 -log(u)/rate, "
+                                           "every lane, full occupancy)" if draw_peak else "derived"),
+                              derived_issue_peak=derived_peak),
                 gpu_launches=r["launches"], clocks=r["clocks"])
-    if not args.no_e2e:
-        e = e2e_sweeps(args, wl, smc, torch, r["h"], r["model"], min(args.steps, 3), world)
-        tot = sum_over_ranks(torch, world, r["alive_steps"] / args.steps)
-    if not args.no_e2e:
+    if wl["model"] == "clads2":
+        line["guard_kills_per_particle_step"] = r["guard"] / max(r["alive_steps"], 1)
+    if with_e2e:
+        e = e2e_sweeps(sub_args, wl, smc, torch, r["h"], r["model"], min(steps, 3), world)
+        tot = sum_over_ranks(torch, world, r["alive_steps"] / steps)
         line["e2e"] = dict(value=tot / e["t"], unit="particle-steps/s",
                            h2d_bytes_per_step=e["h2d"] * world, d2h_bytes_per_step=e["d2h"] * world,
                            note="per step: H2D of the model data, reset(seed), run, D2H of log Z and "
                                 "the final log-weights; host wall clock, max over ranks")
-    if rank == 0 and not args.no_cpu_baseline and world == 1:
+    if rank == 0 and with_cpu and world == 1:
         v, sample, dt, _ = oracle_sweep_rate(wl, budget_s=args.cpu_budget)
         line["cpu_baseline"] = dict(value=v, unit="particle-steps/s", cores=1, kind="oracle",
-                                    sample=sample, seconds=dt)
-    if rank == 0:
-        print(json.dumps(line), flush=True)
+                                    sample=sample, seconds=dt, host=host_cpu())
+    r["h"].close()
+    oracle_sweep_rate.ess = args.ess
+    return line
+
+
+def host_cpu():
+    """lscpu model name and nproc of the box."""
+    model = ""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:  # noqa: BLE001
+        pass
+    return dict(model=model, nproc=os.cpu_count())
 
 
 def main():
@@ -598,6 +692,8 @@ def main():
     ap.add_argument("--inplace", action="store_true",
                     help="in-place resampling by ancestor permutation (DESIGN R-21, SURVEY f3)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--only", action="store_true",
+                    help="default workload: skip the configs[2]-[4] sub-results")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out"))

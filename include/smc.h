@@ -304,6 +304,16 @@ int smc_last_distinct(smc_handle h, uint64_t* out);
 int smc_plan_ranges(const uint64_t* w_lohi, int32_t world, uint64_t n_per, uint64_t z,
                     uint64_t* out);
 
+/* Measured draw-rate ceiling of propagation (the roofline
+ * denominator of the "alu"-bound propagation kernels): launches a
+ * divergence-free microkernel on the current device in which every lane of a
+ * full-occupancy grid draws draws_per_thread Exp(rate) variates from its own
+ * Philox4x32-10 stream (hq conversion, fp64 -log(u)/rate; R-1..R-3)
+ * and writes their sum.  *draws_per_s = uniforms consumed per second, best of
+ * three timed launches (CUDA events).  SMC_EINVAL for a NULL output or 0
+ * draws; SMC_ECUDA without a device.  Allocates and frees its own buffer. */
+int smc_draw_peak(uint32_t draws_per_thread, double* draws_per_s);
+
 /* Symbols-only helper: ABI version of the loaded library. */
 int smc_abi_version(void);
 

@@ -72,6 +72,7 @@ class smc_comm(C.Structure):
 H = C.c_void_p
 _sig = {
     "smc_abi_version": ([], C.c_int),
+    "smc_draw_peak": ([C.c_uint32, C.POINTER(C.c_double)], C.c_int),
     "smc_create": ([C.POINTER(smc_model), C.c_uint64, C.c_uint64], H),
     "smc_create_virtual": ([C.POINTER(smc_model), C.c_uint64, C.c_uint64, C.c_int32], H),
     "smc_create_sharded": ([C.POINTER(smc_model), C.c_uint64, C.c_uint64, C.c_int32, C.c_int32,
@@ -400,6 +401,14 @@ def plan_ranges(shard_totals, n_per: int, z: int):
     _check(None, _lib.smc_plan_ranges(w.ctypes.data_as(C.POINTER(C.c_uint64)), world, int(n_per),
                                       int(z), out.ctypes.data_as(C.POINTER(C.c_uint64))))
     return [int(v) for v in out]
+
+
+def draw_peak(draws_per_thread: int = 2048) -> float:
+    """Measured draw-rate ceiling (uniforms/s) of the current device: the
+    divergence-free Philox + hq + fp64 Exp microkernel (smc_draw_peak)."""
+    v = C.c_double(0.0)
+    _check(None, _lib.smc_draw_peak(int(draws_per_thread), C.byref(v)))
+    return v.value
 
 
 def aos_to_soa(states: np.ndarray) -> np.ndarray:

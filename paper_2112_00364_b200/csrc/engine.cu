@@ -924,12 +924,58 @@ smc_ctx* finish_create(smc_ctx* h, int rc) {
   return nullptr;
 }
 
+// Draw-rate ceiling of propagation: every lane draws D
+// Exp(rate) variates from its own Philox stream (hq conversion, fp64 log and
+// division: the minimal work of one uniform consumed by a sampler), with no
+// divergence, no memory traffic and full occupancy.
+__global__ void __launch_bounds__(256) draw_peak_kernel(unsigned draws, double* out) {
+  const uint32_t gid = blockIdx.x * blockDim.x + threadIdx.x;
+  Rng r(0x5EEDull, gid, 0u);
+  double acc = 0.0, rate = 1.0 + 1e-3 * (double)(threadIdx.x & 7);
+  for (unsigned d = 0; d < draws; ++d) acc += d_exp(r, rate);
+  out[gid] = acc;
+}
+
 }  // namespace
 
 // ============================================================================
 // C ABI
 // ============================================================================
 extern "C" {
+
+int smc_draw_peak(uint32_t draws_per_thread, double* draws_per_s) {
+  smc_ctx* h = nullptr;
+  if (!draws_per_s || draws_per_thread == 0) return fail(h, SMC_EINVAL, "bad argument");
+  int dev = 0, sms = 0, per_sm = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, draw_peak_kernel, 256, 0));
+  const unsigned grid = (unsigned)(sms * std::max(per_sm, 1));
+  double* out = nullptr;
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  CU(cudaMalloc(&out, (size_t)grid * 256 * sizeof(double)));
+  CU(cudaEventCreate(&e0));
+  CU(cudaEventCreate(&e1));
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {           // first launch warms up
+    CU(cudaEventRecord(e0, st));
+    draw_peak_kernel<<<grid, 256, 0, st>>>(draws_per_thread, out);
+    CU(cudaEventRecord(e1, st));
+    CU(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, e0, e1));
+    if (rep) best = std::min(best, ms);
+  }
+  CU(cudaGetLastError());
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  cudaStreamDestroy(st);
+  *draws_per_s = (double)grid * 256.0 * (double)draws_per_thread / (best * 1e-3);
+  return SMC_OK;
+}
 
 int smc_abi_version(void) { return SMC_ABI_VERSION; }
 

@@ -457,6 +457,7 @@ __global__ void __launch_bounds__(kLRThreads, M::kLRMinBlocks) propagate_lr_kern
         drw += 2;
         NodeOut out;
         const int res = M::node(ts, tl, tidv, s_own[o], n_owner, epoch, seed, rho, out);
+        if (M::kHasLam && (res == NODE_BIRTH || res == NODE_GUARD)) drw += 2;   // daughters' noise block
         if (res == NODE_DETECTED || res == NODE_GUARD) {
           atomicCAS(&s_dead[o], 0, res == NODE_GUARD ? 3 : 1);
         } else if (res == NODE_BIRTH) {
