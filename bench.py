@@ -602,10 +602,26 @@ def sweep_line(args, name, wl, smc, torch, world, rank, pk, pk_kind, draw_peak, 
     prop_s = max(r["prop_ms"] / steps * 1e-3, 1e-12)
     gpu_rate = r["draws"] / steps / prop_s / 1e9
     lin = rng == "lineage" and not wl.get("analytic")
-    try:
-        odps, osample = oracle_draws_per_step(wl, n=20000 if wl["model"] != "seir" else 5000)
-    except Exception as e:  # noqa: BLE001  (the oracle is a reported baseline, not the product)
-        odps, osample = None, f"oracle unavailable: {e}"
+    gdps = r["draws"] / max(r["alive_steps"], 1)
+    cpu = None
+    if rank == 0 and with_cpu and world == 1:
+        cpu = oracle_sweep_rate(wl, budget_s=args.cpu_budget)
+    if lin:
+        # speculative side-tree nodes inflate the GPU's count: the algorithmic
+        # count is the oracle's, on a sample of the same workload (the
+        # cpu_baseline sweep when it ran, else a 20000-particle sweep)
+        try:
+            if cpu:
+                odps = cpu[3]["draws"] / max(cpu[3]["alive_particle_steps"], 1)
+                osample = cpu[1]
+            else:
+                odps, osample = oracle_draws_per_step(wl, n=20000)
+        except Exception as e:  # noqa: BLE001  (the oracle is a reported baseline, not the product)
+            odps, osample = None, f"oracle unavailable: {e}"
+    else:
+        # identical streams: the GPU draws exactly the oracle's uniforms
+        # (tests/test_gpu_fullsweep.py asserts equality at 10^6)
+        odps, osample = gdps, "equal to the GPU count (identical streams, asserted at 10^6 in tests)"
     alg_rate = (odps * r["alive_steps"] / steps / prop_s / 1e9) if odps else None
     peak = draw_peak if draw_peak else derived_peak
     prop_frac = r["prop_ms"] / max(r["prop_ms"] + r["res_ms"], 1e-9)
@@ -623,8 +639,7 @@ def sweep_line(args, name, wl, smc, torch, world, rank, pk, pk_kind, draw_peak, 
                 resamples_per_sweep=r["resamples_per_sweep"],
                 phase_ms=dict(propagate=r["prop_ms"] / steps, resample=r["res_ms"] / steps,
                               propagate_share=prop_frac),
-                draws_per_particle_step=dict(oracle=odps, oracle_sample=osample,
-                                             gpu=r["draws"] / max(r["alive_steps"], 1),
+                draws_per_particle_step=dict(oracle=odps, oracle_sample=osample, gpu=gdps,
                                              note="gpu counts speculative side-tree nodes (R-18)"
                                              if lin else "identical streams"),
                 resample_roofline=dict(bound="hbm", achieved=r["res_bytes"] / (r["res_ms"] * 1e-3) / 1e9,
@@ -652,8 +667,8 @@ def sweep_line(args, name, wl, smc, torch, world, rank, pk, pk_kind, draw_peak, 
                            h2d_bytes_per_step=e["h2d"] * world, d2h_bytes_per_step=e["d2h"] * world,
                            note="per step: H2D of the model data, reset(seed), run, D2H of log Z and "
                                 "the final log-weights; host wall clock, max over ranks")
-    if rank == 0 and with_cpu and world == 1:
-        v, sample, dt, _ = oracle_sweep_rate(wl, budget_s=args.cpu_budget)
+    if cpu:
+        v, sample, dt, _ = cpu
         line["cpu_baseline"] = dict(value=v, unit="particle-steps/s", cores=1, kind="oracle",
                                     sample=sample, seconds=dt, host=host_cpu())
     r["h"].close()

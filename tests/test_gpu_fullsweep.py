@@ -8,8 +8,10 @@ CRBD and ClaDS at 10^6 particles per GPU match the oracle.
 Compared: final log Z (relative 1e-9), the final log-weights (relative 1e-9,
 -inf pattern exact), the last resample's ancestors (bit-exact), every state
 field (pc exact, floats relative 1e-9), and the run statistics (epochs,
-resamples, alive particle-steps, helper-cap overflows, ClaDS2 rate-guard kills
-for the sequential reading, where they are schedule-independent).
+resamples, alive particle-steps, helper-cap overflows, uniforms drawn: equal
+for the sequential streams; ClaDS2 rate-guard
+kills within a factor 2 under R-18, where their attribution is schedule-
+dependent).
 
 The four oracle sweeps (about 2-4 minutes each on one core) start together on
 host threads when the first test needs them (ctypes releases the GIL).
@@ -81,6 +83,12 @@ def test_whole_sweep_10e6_vs_oracle(smc, oracle_sweeps, name):
     assert sg["epochs"] == so["epochs"] and sg["resamples"] == so["resamples"]
     assert sg["alive_particle_steps"] == so["alive_particle_steps"]
     assert sg["overflow"] == so["overflow"] == 0
+    if "lineage" not in name:
+        # identical streams: the GPU draws exactly the oracle's uniforms
+        # (bench.py uses this count as the algorithmic work).  Under R-18 the
+        # count depends on the visiting order (a detection found earlier or
+        # later prunes a different number of side-tree nodes): not compared.
+        assert sg["draws"] == so["draws"]
     if name == "clads2_lineage":
         # under R-18 a step whose side trees both detect and break the guard
         # may be attributed either way: only the order of magnitude is fixed
