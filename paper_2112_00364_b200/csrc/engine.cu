@@ -26,6 +26,7 @@
 #include "smc.h"
 #include "kernels.cuh"
 #include "lineage.cuh"
+#include "lineage_warp.cuh"
 
 using namespace smc;
 
@@ -97,6 +98,7 @@ struct smc_ctx {
   U192* d_blk_q2 = nullptr;       // [fused_grid]
   bool stack_prefix = true;       // §R-22 copy only the used stack prefix (env SMC_NO_STACK_PREFIX=1: off, diagnostics)
   int lr_grid = 0;                // persistent grid of the cooperative kernel
+  bool lr_warp = true;            // warp-level cooperative kernel (env SMC_LR_KERNEL=cta: CTA rounds)
   int prop_grid = 0;              // resident-CTA grid of propagate_kernel<M> (grid-stride)
   TaskArrays tasks{};
   int planes = 0;                 // 16-byte planes per particle
@@ -523,17 +525,26 @@ int common_init(smc_ctx* h, const smc_model* m, unsigned long long n_per, int wo
   CU(cudaMalloc(&h->d_barrier, sizeof(int)));
   CU(cudaMallocHost(&h->h_ctrl, sizeof(Ctrl)));
   if (h->lineage) {
+    const char* ek = std::getenv("SMC_LR_KERNEL");
+    h->lr_warp = !(ek && std::strcmp(ek, "cta") == 0);
     int per_sm = 0;
-    if (h->kind == SMC_CRBD)
+    if (h->lr_warp) {
+      if (h->kind == SMC_CRBD)
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, propagate_lrw_kernel<CrbdLR>, kWThreads, 0));
+      else
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, propagate_lrw_kernel<Clads2LR>, kWThreads, 0));
+    } else if (h->kind == SMC_CRBD) {
       CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, propagate_lr_kernel<CrbdLR>, kLRThreads, 0));
-    else
+    } else {
       CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, propagate_lr_kernel<Clads2LR>, kLRThreads, 0));
+    }
     int dev = 0, sms = 0;
     CU(cudaGetDevice(&dev));
     CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const unsigned long long batches = (n_per + kOwners - 1) / kOwners;
+    const unsigned long long per_batch = h->lr_warp ? 32ull * kWWarps : (unsigned long long)kOwners;
+    const unsigned long long batches = (n_per + per_batch - 1) / per_batch;
     h->lr_grid = (int)std::min<unsigned long long>(batches, (unsigned long long)std::max(1, per_sm) * sms);
-    h->tasks.cap = kTasksPerCta;
+    h->tasks.cap = h->lr_warp ? (unsigned)(kWWarps * kTasksPerWarp) : kTasksPerCta;
     const size_t nt = (size_t)h->lr_grid * h->tasks.cap;
     CU(cudaMalloc(&h->tasks.sid, nt * sizeof(double2)));
     if (h->kind == SMC_CLADS2) CU(cudaMalloc(&h->tasks.lam, nt * sizeof(double)));
@@ -630,6 +641,11 @@ void launch_prop_lr(smc_ctx* h, Shard& s, int cur) {
   a.p.rank = s.id;
   a.p.ctrl = s.ctrl;
   a.t = h->tasks;
+  if (h->lr_warp) {
+    a.n_batches = (unsigned)((h->n_per + 31) / 32);
+    propagate_lrw_kernel<M><<<h->lr_grid, kWThreads, 0, h->stream>>>(a, h->mc);
+    return;
+  }
   a.n_batches = (unsigned)((h->n_per + kOwners - 1) / kOwners);
   propagate_lr_kernel<M><<<h->lr_grid, kLRThreads, 0, h->stream>>>(a, h->mc);
 }

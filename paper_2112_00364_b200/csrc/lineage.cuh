@@ -86,6 +86,7 @@ struct OwnerClads2 { double eps, alpha, sigma, pb; };
 // ---------------------------------------------------------------------------
 struct CrbdLR {
   static constexpr int kLRMinBlocks = SMC_LR_MINB;   // 64 registers at 128 threads
+  static constexpr int kLRWMinBlocks = 8;            // warp-level kernel (lineage_warp.cuh)
   typedef Crbd::State State;
   typedef OwnerCrbd Owner;
   static constexpr int kPlanes = Crbd::kPlanes;
@@ -156,6 +157,10 @@ struct Clads2LR {
 #define SMC_LR_MINB_CLADS2 4
 #endif
   static constexpr int kLRMinBlocks = SMC_LR_MINB_CLADS2;   // larger state: avoid spills
+#ifndef SMC_LRW_MINB_CLADS2
+#define SMC_LRW_MINB_CLADS2 4
+#endif
+  static constexpr int kLRWMinBlocks = SMC_LRW_MINB_CLADS2;
   typedef Clads2::State State;
   typedef OwnerClads2 Owner;
   static constexpr int kPlanes = Clads2::kPlanes;

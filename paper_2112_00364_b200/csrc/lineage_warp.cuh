@@ -1,0 +1,286 @@
+// lineage_warp.cuh — warp-independent cooperative propagation for the
+// birth-death models under the lineage-keyed side-tree reading (DESIGN.md
+// §R-18, §7.1).
+//
+// Same work as propagate_lr_kernel (lineage.cuh): phase 1 walks each
+// particle's observed branch on its own stream and pushes one root task per
+// hidden event; phase 2 evaluates the hidden side trees cooperatively (every
+// tree node is one Philox block, so nodes may be evaluated in any order);
+// phase 3 finishes the particle (-inf if any node was detected, else + ln 2 per
+// hidden event).  The difference is the unit of cooperation: each WARP pulls
+// its own batch of 32 particles and runs the rounds warp-synchronously —
+// counts, fair-share lane assignment, detection flags and pushes go through
+// registers, shuffles and per-warp shared memory with __syncwarp only.  No CTA
+// barrier sits inside the loop, so a warp stuck on a deep side tree holds back
+// nobody, and a round costs a few dozen instructions instead of four CTA
+// barriers (ncu, profiles/r02: the CTA rounds were ~40% of the instructions
+// and half of the stall samples of the CTA version).
+//
+// Per round: every owner lane with c pending tasks offers its top
+// m = min(c, max(1, 32 / #busy owners)) tasks (LIFO: depth-first per owner, so
+// a supercritical tree is detected along one path); lanes are assigned by an
+// exclusive scan of m; lanes left over pop the warp's overflow stack.  Owner
+// state (task count, detection flag, node count, lw, number of hidden events)
+// lives in the owner lane's registers for the whole batch.
+#pragma once
+#include "lineage.cuh"
+
+namespace smc {
+
+#ifndef SMC_LRW_THREADS
+#define SMC_LRW_THREADS 128
+#endif
+constexpr int kWThreads = SMC_LRW_THREADS;       // CTA = kWThreads / 32 independent warps
+constexpr int kWWarps = kWThreads / 32;
+constexpr int kWSeg = 256;                       // per-owner LIFO segment (tasks)
+constexpr int kWOvf = 1 << 16;                   // per-warp overflow LIFO (tasks)
+constexpr unsigned long long kWSegSlots = 32ull * kWSeg;
+constexpr unsigned long long kTasksPerWarp = kWSegSlots + kWOvf;
+
+template <class M>
+__global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_kernel(LRArgs a, ModelConst C) {
+  __shared__ typename M::Owner s_own[kWWarps][32];   // per-owner constants read by every lane
+  __shared__ int s_start[kWWarps][32];               // round: lane where owner o's tasks start
+  __shared__ int s_push[kWWarps][32];                // round: slots pushed for owner o
+  __shared__ int s_det[kWWarps][32];                 // round: 1 detected, 3 rate guard
+  __shared__ int s_ovn[kWWarps][32];                 // round: overflow tasks of owner o evaluated
+  __shared__ int s_ovtop[kWWarps];                   // overflow stack top
+  __shared__ int s_taskcap;
+  __shared__ long long s_key[kWWarps];
+  __shared__ unsigned long long s_acc[3][kWWarps];
+  const PropArgs& p = a.p;
+  if (*(volatile unsigned*)&p.ctrl->done) return;
+  constexpr unsigned FULL = 0xffffffffu;
+  const unsigned epoch = p.ctrl->epoch;
+  const unsigned long long seed = p.ctrl->seed;
+  const bool carry = p.ctrl->carry != 0;
+  const double rho = C.p[0];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned long long tbase = ((unsigned long long)blockIdx.x * kWWarps + warp) * kTasksPerWarp;
+  double2* T_sid = a.t.sid + tbase;
+  double* T_lam = M::kHasLam ? a.t.lam + tbase : nullptr;
+  unsigned short* T_own = a.t.owner + tbase;
+  if (threadIdx.x == 0) s_taskcap = 0;
+  __syncthreads();
+
+  auto put = [&](unsigned long long slot, double s0, double lam0, unsigned long long id) {
+    T_sid[slot] = make_double2(s0, __longlong_as_double((long long)id));
+    if (M::kHasLam) T_lam[slot] = lam0;
+  };
+  // overflow slot for owner o (-1: the warp's stack is full -> task-cap error)
+  auto ovf_slot = [&](int o) -> long long {
+    const int q = atomicAdd(&s_ovtop[warp], 1);
+    if (q >= kWOvf) { s_taskcap = 1; return -1; }
+    const unsigned long long slot = kWSegSlots + (unsigned long long)q;
+    T_own[slot] = (unsigned short)o;
+    return (long long)slot;
+  };
+
+  long long key = LLONG_MIN;
+  unsigned long long n_end = 0, n_start = 0, drw = 0, ovf = 0, roots = 0, guard = 0;
+  bool bad = false;
+  unsigned max_rounds = 0, max_nodes = 0;
+
+  for (;;) {
+    unsigned batch = 0;
+    if (lane == 0) {
+      batch = atomicAdd(&p.ctrl->batch, 1u);
+      s_ovtop[warp] = 0;
+    }
+    batch = __shfl_sync(FULL, batch, 0);
+    if (batch >= a.n_batches) break;
+    const unsigned long long bbase = (unsigned long long)batch * 32;
+    const unsigned long long i = bbase + lane;
+    const bool valid = i < p.n_local;
+    // ---------------- phase 1: the particle's own stream (owner = this lane)
+    int c = 0;                       // tasks in this owner's segment
+    int dead = 0;                    // 0 alive, 1 detected, 2 node cap, 3 rate guard
+    unsigned nodes = 0;
+    double lw = (valid && carry) ? p.lw[i] : 0.0;   // R-19 carried weights
+    int K = 0;
+    bool act = false, alive_end = false;
+    __syncwarp();
+    if (valid) {
+      typename M::State st;
+      M::load(st, p.planes, p.n_local, i);
+      if (M::pc(st) != kStop) {
+        act = true;
+        ++n_start;
+        Rng r(seed, (uint32_t)(p.shard_base + i), epoch);
+        auto push = [&](double s0, double lam0, unsigned kk) {
+          long long slot;
+          if (c < kWSeg) slot = (long long)lane * kWSeg + c++;
+          else slot = ovf_slot(lane);
+          if (slot >= 0) put((unsigned long long)slot, s0, lam0, root_id(kk));
+        };
+        if (!M::main_part(st, lw, r, C, s_own[warp][lane], K, push)) dead = 3;   // rate guard
+        roots += (unsigned long long)K;
+        drw += 2ull * r.blk - (r.has_spare ? 1ull : 0ull);
+        M::store(st, p.planes, p.n_local, i);
+      }
+      alive_end = M::pc(st) != kStop;
+    }
+    __syncwarp();
+    // ---------------- phase 2: warp-synchronous rounds
+    unsigned rounds = 0;
+    for (;;) {
+      if (dead) c = 0;                                  // a dead owner drops its stack
+      const int ov = min(*(volatile int*)&s_ovtop[warp], kWOvf);
+      const int n_act = __popc(__ballot_sync(FULL, c > 0));
+      if (n_act == 0 && ov == 0) break;
+      // fair share: a heuristic (no result depends on the schedule, R-18)
+      const int W = n_act ? max(1, 32 / n_act) : 0;
+      const int m = min(c, W);
+      int incl = m;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(FULL, incl, d);
+        if (lane >= d) incl += t;
+      }
+      const int off = incl - m;
+      const int T = min(__shfl_sync(FULL, incl, 31), 32);
+      const int me = max(0, min(m, 32 - off));
+      s_start[warp][lane] = -1;
+      s_push[warp][lane] = 0;
+      s_det[warp][lane] = 0;
+      s_ovn[warp][lane] = 0;
+      __syncwarp();
+      if (me > 0) s_start[warp][off] = lane;
+      __syncwarp();
+      int o = s_start[warp][lane];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {               // owner of lane = last start at or below it
+        const int t = __shfl_up_sync(FULL, o, d);
+        if (lane >= d) o = max(o, t);
+      }
+      // lane -> task: own-segment tasks first (lanes [0, T)), then the overflow stack
+      const int osrc = max(o, 0);
+      const int c_o = __shfl_sync(FULL, c, osrc);
+      const int off_o = __shfl_sync(FULL, off, osrc);
+      bool have = false;
+      unsigned long long slot = 0;
+      int ow = 0;
+      if (lane < T) {
+        have = true;
+        ow = o;
+        slot = (unsigned long long)o * kWSeg + (unsigned long long)(c_o - 1 - (lane - off_o));
+      } else if (lane - T < ov) {
+        have = true;
+        slot = kWSegSlots + (unsigned long long)(ov - 1 - (lane - T));
+        ow = (int)T_own[slot];
+      }
+      c -= me;                                          // pops (the owner's base for pushes)
+      const int base_ow = __shfl_sync(FULL, c, ow);
+      const int dead_ow = __shfl_sync(FULL, dead, ow);
+      const bool run = have && dead_ow == 0;
+      // read the popped records before any lane pushes: pushes reuse the
+      // popped slots (segment: from the owner's base up; overflow: from the
+      // new top up)
+      double2 rec = make_double2(0.0, 0.0);
+      double tl = 0.0;
+      if (run) {
+        rec = T_sid[slot];
+        if (M::kHasLam) tl = T_lam[slot];
+      }
+      if (lane == 0) s_ovtop[warp] = ov - min(ov, 32 - T);
+      __syncwarp();
+      if (run) {
+        if (slot >= kWSegSlots) atomicAdd(&s_ovn[warp][ow], 1);
+        const uint32_t n_owner = (uint32_t)(p.shard_base + bbase + ow);
+        drw += 2;
+        NodeOut out;
+        const int res = M::node(rec.x, tl, (unsigned long long)__double_as_longlong(rec.y), s_own[warp][ow],
+                                n_owner, epoch, seed, rho, out);
+        if (M::kHasLam && (res == NODE_BIRTH || res == NODE_GUARD)) drw += 2;   // daughters' noise block
+        if (res == NODE_DETECTED || res == NODE_GUARD) {
+          atomicCAS(&s_det[warp][ow], 0, res == NODE_GUARD ? 3 : 1);
+        } else if (res == NODE_BIRTH) {
+          const int b = base_ow + atomicAdd(&s_push[warp][ow], 2);
+          const long long s1 = b < kWSeg ? (long long)ow * kWSeg + b : ovf_slot(ow);
+          const long long s2 = b + 1 < kWSeg ? (long long)ow * kWSeg + b + 1 : ovf_slot(ow);
+          if (s1 >= 0) put((unsigned long long)s1, out.s2, out.lb, out.idb);
+          if (s2 >= 0) put((unsigned long long)s2, out.s2, out.la, out.ida);   // first daughter on top
+        }
+      }
+      __syncwarp();
+      // owner updates
+      if (dead == 0) {
+        nodes += (unsigned)(me + s_ovn[warp][lane]);
+        const int dc = s_det[warp][lane];
+        if (dc) dead = dc;
+        else if (nodes > kSideNodeCap) dead = 2;
+      }
+      c = min(c + s_push[warp][lane], kWSeg);
+      ++rounds;
+      __syncwarp();
+    }
+    max_rounds = rounds > max_rounds ? rounds : max_rounds;
+    max_nodes = nodes > max_nodes ? nodes : max_nodes;
+    // ---------------- phase 3: finish the particle
+    if (valid) {
+      double w = lw;
+      if (act) {
+        if (dead) {
+          w = -INFINITY;
+          if (dead == 3) ++guard;
+          if (dead == 2) {
+            ++ovf;
+            atomicMin(&p.ctrl->first_err, (unsigned long long)(p.shard_base + i));
+          }
+        } else {
+          for (int k = 0; k < K; ++k) w = w + kLn2;
+        }
+      }
+      p.lw[i] = w;
+      if (alive_end) ++n_end;
+      bad |= isnan(w) || w == INFINITY;
+      const long long kk = order_key(w);
+      key = kk > key ? kk : key;
+    }
+  }
+  // ---------------- epilogue: warp sums, then one set of atomics per CTA
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const long long t = __shfl_xor_sync(FULL, key, d);
+    key = t > key ? t : key;
+    n_end += __shfl_xor_sync(FULL, n_end, d);
+    n_start += __shfl_xor_sync(FULL, n_start, d);
+    drw += __shfl_xor_sync(FULL, drw, d);
+    ovf += __shfl_xor_sync(FULL, ovf, d);
+    roots += __shfl_xor_sync(FULL, roots, d);
+    guard += __shfl_xor_sync(FULL, guard, d);
+    max_nodes = max(max_nodes, __shfl_xor_sync(FULL, max_nodes, d));
+  }
+  bad = __any_sync(FULL, bad);
+  if (lane == 0) {
+    s_key[warp] = key;
+    s_acc[0][warp] = n_end;
+    s_acc[1][warp] = n_start;
+    s_acc[2][warp] = drw;
+    if (ovf) atomicAdd(&p.ctrl->overflow, ovf);
+    if (guard) atomicAdd(&p.ctrl->guard_kills, guard);
+    if (roots) atomicAdd(&p.ctrl->side_roots, roots);
+    atomicMax(&p.ctrl->max_side_nodes, max_nodes);
+    atomicMax(&p.ctrl->max_rounds, max_rounds);
+  }
+  const int any_bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    long long k = s_key[0];
+    unsigned long long e = 0, st = 0, dr = 0;
+    for (int w = 0; w < kWWarps; ++w) {
+      k = s_key[w] > k ? s_key[w] : k;
+      e += s_acc[0][w];
+      st += s_acc[1][w];
+      dr += s_acc[2][w];
+    }
+    RecA* rec = p.recA + (epoch & 1) * p.world + p.rank;
+    atomicMax(&rec->key, k);
+    if (e) atomicAdd(&rec->alive, (unsigned)e);
+    if (any_bad) atomicOr(&rec->flags, 1u);
+    if (s_taskcap) atomicOr(&rec->flags, 2u);
+    if (st) atomicAdd(&p.ctrl->alive_steps, st);
+    if (dr) atomicAdd(&p.ctrl->draws, dr);
+  }
+}
+
+}  // namespace smc
