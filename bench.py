@@ -47,6 +47,10 @@ WORKLOADS = {
                            "different epochs (universal control flow, SURVEY f4)"),
     "ssm": dict(config=None, model="ssm", n=1_000_000,
                 desc="linear-Gaussian state-space model, Eq. (2), 50 synthetic observations (SURVEY f4)"),
+    "fig3": dict(config=None, model="fig3", n=1_000_000,
+                 desc="the PCFG of Fig. 3(a): five blocks with jumps, a self-loop and checkpoints; "
+                      "particles at different blocks within an epoch and stopping at different "
+                      "epochs (SURVEY f4, DESIGN R-23)"),
     "resample": dict(config=4, model="resample", n=1 << 26,
                      desc="resampling step alone: LSE max + u128 scan + systematic ancestors + 64-B gather"),
 }
@@ -147,6 +151,8 @@ def model_for(smc, wl, rng="lineage", inplace=False):
         return smc.Model.geometric(*inputs.GEOMETRIC_PARAMS, flags=fl)
     if wl["model"] == "ssm":
         return smc.Model.ssm(inputs.ssm_series(50), inputs.SSM_PARAMS, flags=fl)
+    if wl["model"] == "fig3":
+        return smc.Model.fig3(*inputs.FIG3_PARAMS, flags=fl)
     raise ValueError(wl)
 
 
@@ -159,12 +165,14 @@ def oracle_sweep_rate(wl, budget_s=15.0, n_cap=None):
     lin = getattr(oracle_sweep_rate, "rng", "lineage") == "lineage"
     kind = {"crbd": (oracle.CRBD_AE if wl.get("analytic") else oracle.CRBD_LR if lin else oracle.CRBD),
             "clads2": oracle.CLADS2_LR if lin else oracle.CLADS2, "seir": oracle.SEIR,
-            "geometric": oracle.GEOMETRIC, "ssm": oracle.SSM}[wl["model"]]
+            "geometric": oracle.GEOMETRIC, "ssm": oracle.SSM, "fig3": oracle.FIG3}[wl["model"]]
     if wl["model"] in ("crbd", "clads2"):
         data = oracle.tree_blob(inputs.tree(wl["tree"]))
         params = inputs.CRBD_PARAMS if wl["model"] == "crbd" else inputs.CLADS2_PARAMS
     elif wl["model"] == "geometric":
         data, params = None, inputs.GEOMETRIC_PARAMS
+    elif wl["model"] == "fig3":
+        data, params = None, inputs.FIG3_PARAMS
     elif wl["model"] == "ssm":
         data, params = inputs.ssm_series(50), inputs.SSM_PARAMS
     else:

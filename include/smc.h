@@ -63,6 +63,8 @@ typedef enum {
   SMC_GEOMETRIC = 10,      /* weighted geometric, Fig. 2                    */
   SMC_SSM = 11,            /* linear-Gaussian state-space model, Eq. (2) / Fig. 4  */
   SMC_CONSTW = 12,         /* weight(log w); checkpoint; ... K times                   */
+  SMC_FIG3 = 13,           /* the PCFG of Fig. 3(a), blocks b0..b4 (DESIGN R-23)    */
+  SMC_STACKF = 14,         /* Fig. 5(c) recursion with a PSTATE byte stack (R-24)   */
   SMC_RESAMPLE_BENCH = 20  /* no blocks: resampler only, opaque state (BASELINE configs[4])    */
 } smc_model_kind;
 
@@ -102,6 +104,17 @@ typedef enum {
  *                exposed humans, [9] initial infectious mosquitoes.
  *  SSM           data = y[T]; params [m0, s0, drift, q, r] (std devs).
  *  GEOMETRIC     params [p, w].      CONSTW  params [log w, K].
+ *  FIG3          params [p_loop, p3, w1, w2, w3, w4] (defaults 0.5, 0.3, 2,
+ *                1.2, 1.2, 0.5): b2 loops with probability p_loop (weight w2),
+ *                goes to b3 with p3 (weight w3, checkpoint, back to b2), else
+ *                to b4 (weight w4, checkpoint, b_stop); b1 weighs w1.
+ *  STACKF        data = y[D] (observation per recursion depth, may be empty);
+ *                params [p0, p_rec, sigma, cap] (defaults 2, 2, 0.5, 768):
+ *                the recursive f of Fig. 5 made terminating (recurse iff
+ *                s1 >= 1), a byte stack of cap bytes (multiple of 16, 48-byte
+ *                frames) plus a stack pointer; state = 16-byte header +
+ *                cap/16 stack planes, of which resampling copies only the
+ *                planes below the stack pointer.
  *  RESAMPLE_BENCH state_bytes = bytes per particle (multiple of 16, <= 512).
  */
 typedef struct {

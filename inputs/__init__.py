@@ -34,6 +34,10 @@ def ssm_series(T: int = 10) -> np.ndarray:
     return np.asarray(_load(f"ssm{T}.json")["y"], dtype=np.float64)
 
 
+def stackf_series(name: str = "stackf12") -> np.ndarray:
+    return np.asarray(_load(f"{name}.json")["y"], dtype=np.float64)
+
+
 def resample_lw(n: int, sigma: float = 1.0, frac_neg_inf: float = 0.0, seed: int = 4) -> np.ndarray:
     """C4 log-weights: lw_k = sigma * N(0,1); a fraction set to -inf."""
     g = np.random.Generator(np.random.PCG64(seed))
@@ -56,3 +60,5 @@ CLADS2_PARAMS = [1.0, -1.0, -1.0, -1.0, -1.0]   # rho, lambda0, sigma, alpha, ep
 SSM_PARAMS = [0.0, 100.0, 2.0, 1.0, 5.0]        # m0, s0, drift, q, r (std devs)
 GEOMETRIC_PARAMS = [0.5, 1.5]                   # p, w  (Fig. 2)
 CONSTW_PARAMS = [float(np.log(3.0)), 4.0]       # log w, K checkpoints
+FIG3_PARAMS = [0.5, 0.3, 2.0, 1.2, 1.2, 0.5]    # p_loop, p3, w1, w2, w3, w4 (Fig. 3(a) PCFG)
+STACKF_PARAMS = [2.0, 2.0, 0.5, 768.0]          # p0, p_rec, sigma, stack bytes (Fig. 5(c) program)

@@ -24,7 +24,8 @@ _lock = threading.Lock()
 _lib = None
 
 # model kinds (same numbering as the public header, redeclared here on purpose)
-CRBD, CLADS2, SEIR, CRBD_LR, CLADS2_LR, CRBD_AE, GEOMETRIC, SSM, CONSTW = 1, 2, 3, 4, 5, 6, 10, 11, 12
+CRBD, CLADS2, SEIR, CRBD_LR, CLADS2_LR, CRBD_AE, GEOMETRIC, SSM, CONSTW, FIG3, STACKF = (
+    1, 2, 3, 4, 5, 6, 10, 11, 12, 13, 14)
 OK, EINVAL, EREJECTED, ENAN = 0, 1, 4, 5
 DIST = {"exp": 0, "bernoulli": 1, "uniform": 2, "normal": 3, "gamma": 4, "beta": 5, "binomial": 6}
 

@@ -72,8 +72,22 @@ def tree5():
     return t
 
 
+def stackf_series(D=12, seed=14):
+    """Per-recursion-level observations of the STACKF program (DESIGN.md
+    R-24): y_d = 1.3 + 0.3 z_d, z_d standard normal from the oracle's Philox
+    uniforms (tag 2, Box-Muller with the cosine)."""
+    u = oracle.uniforms(seed, 0, 0, 2, 2 * D)
+    z = np.sqrt(-2.0 * np.log(u[0::2])) * np.cos(2.0 * np.pi * u[1::2])
+    y = 1.3 + 0.3 * z
+    with open(os.path.join(ROOT, f"stackf{D}.json"), "w") as f:
+        json.dump(dict(y=y.tolist(), seed=seed,
+                       recipe=f"y_d = 1.3 + 0.3 z_d, d < {D}; z_d Box-Muller of oracle.uniforms("
+                              f"seed={seed}, particle 0, epoch 0, tag 2)"), f, indent=1)
+
+
 def main():
     os.makedirs(ROOT, exist_ok=True)
+    stackf_series()
     t5 = tree5()
     t5["newick"] = newick(t5)
     t5["summary"] = tree_summary(t5)

@@ -756,6 +756,148 @@ struct SeirModel {
   }
 };
 
+// ---- The PCFG of Fig. 3(a) ---------
+// Blocks b0..b4 and b_stop with the figure's transitions; regular arrows are
+// checkpoint transitions, open arrows are not:
+//   b0 -> b1 (ckpt)
+//   b1 -> b2          weight(w1)
+//   b2 -> b2 | b3 | b4  one uniform u: u < p_loop: self-loop with weight(w2);
+//                       u < p_loop + p3: to b3; else to b4 (no checkpoints)
+//   b3 -> b2 (ckpt)   weight(w3)
+//   b4 -> b_stop (ckpt) weight(w4)
+// Particles run different block sequences within one epoch and reach b_stop
+// at different epochs.  State: pc, n (b3 visits), x (b2 loops).
+struct Fig3Model {
+  double p_loop = 0.5, p3 = 0.3, w1 = 2.0, w2 = 1.2, w3 = 1.2, w4 = 0.5;
+  enum { B0 = 0, B1 = 1, B2 = 2, B3 = 3, B4 = 4 };
+  struct State { int pc = 0; int n = 0; int x = 0; };
+  static const int NF = 3;
+  void fields(const State& s, double* f) const { f[0] = s.pc; f[1] = s.n; f[2] = s.x; }
+  int step(State& s, double& lw, Stream& rs, uint64_t&) const {
+    switch (s.pc) {
+      case B0:
+        s.n = 0; s.x = 0; s.pc = B1;
+        return 1;
+      case B1:
+        lw = lw + std::log(w1); s.pc = B2;
+        return 0;
+      case B2: {
+        double u = sample_uniform(rs, 0.0, 1.0);
+        if (u < p_loop) { s.x = s.x + 1; lw = lw + std::log(w2); s.pc = B2; }
+        else if (u < p_loop + p3) s.pc = B3;
+        else s.pc = B4;
+        return 0;
+      }
+      case B3:
+        s.n = s.n + 1; lw = lw + std::log(w3); s.pc = B2;
+        return 1;
+      default:   // B4
+        lw = lw + std::log(w4); s.pc = PC_STOP;
+        return 1;
+    }
+  }
+};
+
+// ---- The compiled recursive function of Fig. 5(c) with a PSTATE stack -------
+// (Fig. 5; Sec. 4.2: "PSTATE consists of a byte array
+// stack and a pointer to the top of this stack"; the part of the
+// stack beyond the stack pointer is not copied)
+// f(p): s1 ~ Gamma(p, 1/p); resample; weight N(y_d; s1, sigma) at recursion
+// depth d (d < |y|); if s1 >= 1 then s4 = f(p_rec); s3 = s4 + s4 else s3 = 8;
+// return s3 * s3.  Blocks as Fig. 5(c): b0 calls f(p0); b1 = block 1 (sample,
+// checkpoint); b2 = block 2 (branch, call); b3 = block 3 (s3 = s4 + s4); b4 =
+// block 4 (return: write s3*s3 at retValLoc, pop, jump to ra).  The frame
+// STACK_f (48 bytes) holds ra, retValLoc (byte offset in the stack; -1: the
+// program's result slot), p, s1, s3, s4.  A push beyond the user-defined stack
+// size (params[3] bytes) sets the weight to -inf (counted as overflow, R-12).
+struct StackfModel {
+  std::vector<double> y;
+  double p0 = 2.0, prec = 2.0, sigma = 0.5;
+  int cap = 768;                                     // stack bytes (multiple of 16)
+  struct Frame { int32_t ra, rv; double p, s1, s3, s4, pad; };
+  static_assert(sizeof(Frame) == 48, "STACK_f is 48 bytes");
+  static const int FRAME = 48;
+  enum { B0 = 0, B1 = 1, B2 = 2, B3 = 3, B4 = 4, RA_STOP = -1 };
+  struct State { int pc = 0; int sp = 0; double result = 0.0; std::vector<uint8_t> stack; };
+  int nf() const { return 3 + 6 * (cap / FRAME); }
+  // stack bytes at or above sp are not part of the state (R-22/R-24): reported as 0
+  void fields(const State& s, double* f) const {
+    f[0] = s.pc; f[1] = s.sp; f[2] = s.result;
+    for (int j = 0; j < cap / FRAME; ++j) {
+      double* g = f + 3 + 6 * j;
+      if ((j + 1) * FRAME <= s.sp) {
+        Frame fr;
+        std::memcpy(&fr, s.stack.data() + j * FRAME, FRAME);
+        g[0] = fr.ra; g[1] = fr.rv; g[2] = fr.p; g[3] = fr.s1; g[4] = fr.s3; g[5] = fr.s4;
+      } else {
+        for (int k = 0; k < 6; ++k) g[k] = 0.0;
+      }
+    }
+  }
+  Frame top(const State& s) const {
+    Frame fr;
+    std::memcpy(&fr, s.stack.data() + s.sp - FRAME, FRAME);
+    return fr;
+  }
+  void set_top(State& s, const Frame& fr) const { std::memcpy(s.stack.data() + s.sp - FRAME, &fr, FRAME); }
+  // push a callee frame; false on stack overflow
+  bool call(State& s, int ra, int rv, double p) const {
+    if (s.sp + FRAME > cap) return false;
+    Frame fr{ra, rv, p, 0.0, 0.0, 0.0, 0.0};
+    std::memcpy(s.stack.data() + s.sp, &fr, FRAME);
+    s.sp = s.sp + FRAME;
+    return true;
+  }
+  int step(State& s, double& lw, Stream& rs, uint64_t& overflow) const {
+    switch (s.pc) {
+      case B0:                                        // main: f(p0), result slot
+        s.stack.assign(cap, 0);
+        s.sp = 0;
+        s.result = 0.0;
+        if (!call(s, RA_STOP, -1, p0)) { ++overflow; lw = -INFINITY; s.pc = PC_STOP; return 1; }
+        s.pc = B1;
+        return 0;
+      case B1: {                                      // s1 = assume Gamma p p; resample
+        Frame fr = top(s);
+        fr.s1 = sample_gamma(rs, fr.p, 1.0 / fr.p);
+        set_top(s, fr);
+        s.pc = B2;
+        return 1;
+      }
+      case B2: {
+        Frame fr = top(s);
+        const int d = s.sp / FRAME - 1;               // recursion depth of this frame
+        if (d < (int)y.size()) lw = lw + normal_logpdf(y[d], fr.s1, sigma);
+        if (fr.s1 >= 1.0) {                           // s4 = f(p_rec)
+          if (!call(s, B3, s.sp - FRAME + 32, prec)) { ++overflow; lw = -INFINITY; s.pc = PC_STOP; return 1; }
+          s.pc = B1;
+        } else {                                      // s3 = 8
+          fr.s3 = 8.0;
+          set_top(s, fr);
+          s.pc = B4;
+        }
+        return 0;
+      }
+      case B3: {                                      // s3 = s4 + s4
+        Frame fr = top(s);
+        fr.s3 = fr.s4 + fr.s4;
+        set_top(s, fr);
+        s.pc = B4;
+        return 0;
+      }
+      default: {                                      // B4: return s3 * s3
+        Frame fr = top(s);
+        const double t = fr.s3 * fr.s3;
+        if (fr.rv < 0) s.result = t;
+        else std::memcpy(s.stack.data() + fr.rv, &t, 8);
+        s.sp = s.sp - FRAME;
+        s.pc = fr.ra == RA_STOP ? PC_STOP : fr.ra;
+        return 0;
+      }
+    }
+  }
+};
+
 // ---- Weighted geometric, Fig. 2(a) ----------------------
 struct GeometricModel {
   double p = 0.5, w = 1.5;
@@ -1001,6 +1143,11 @@ inline void set_side_draws(Clads2LRModel& m, uint64_t* d) { m.draws = d; }
 inline void set_guard(...) {}
 inline void set_guard(Clads2Model& m, uint64_t* g) { m.guard = g; }
 
+// Number of decoded fields: compile-time for most models, run-time (stack size)
+// for the PSTATE-stack model.
+template <class M> struct NfOf { static int get(const M&) { return M::NF; } };
+template <> struct NfOf<StackfModel> { static int get(const StackfModel& m) { return m.nf(); } };
+
 // Adapter: the Alg. 1 loop calls step(); lineage-keyed models need (n, t).
 template <class M> struct StepCall {
   static int call(const M& m, typename M::State& s, double& lw, Stream& rs, uint64_t& ovf,
@@ -1028,9 +1175,10 @@ struct Smc : SmcBase {
     anc.resize(N);
     for (uint64_t j = 0; j < N; ++j) anc[j] = (uint32_t)j;
   }
-  int nfields() const override { return M::NF; }
+  int nfields() const override { return NfOf<M>::get(model); }
   void get_fields(double* out) const override {
-    for (uint64_t n = 0; n < N; ++n) model.fields(st[n], out + n * M::NF);
+    const int nf = NfOf<M>::get(model);
+    for (uint64_t n = 0; n < N; ++n) model.fields(st[n], out + n * nf);
   }
   int step(int* done) override {
     if (finished || status != E_OK) { *done = 1; return status; }
@@ -1116,7 +1264,7 @@ thread_local std::string g_err;
 extern "C" {
 
 enum { K_CRBD = 1, K_CLADS2 = 2, K_SEIR = 3, K_CRBD_LR = 4, K_CLADS2_LR = 5, K_CRBD_AE = 6,
-       K_GEOMETRIC = 10, K_SSM = 11, K_CONSTW = 12 };
+       K_GEOMETRIC = 10, K_SSM = 11, K_CONSTW = 12, K_FIG3 = 13, K_STACKF = 14 };
 
 const char* oracle_errmsg() { return g_err.c_str(); }
 
@@ -1295,6 +1443,24 @@ void* oracle_smc_create(int kind, const double* data, uint64_t data_len,
       if (m.y.empty()) { g_err = "empty series"; return nullptr; }
       m.m0 = P(0, 0.0); m.s0 = P(1, 100.0); m.drift = P(2, 2.0); m.q = P(3, 1.0); m.r = P(4, 5.0);
       return new Smc<SsmModel>(m, N, seed);
+    }
+    case K_FIG3: {
+      Fig3Model m;
+      m.p_loop = P(0, 0.5); m.p3 = P(1, 0.3); m.w1 = P(2, 2.0); m.w2 = P(3, 1.2); m.w3 = P(4, 1.2);
+      m.w4 = P(5, 0.5);
+      if (!(m.p_loop >= 0 && m.p3 >= 0 && m.p_loop + m.p3 <= 1 && m.w1 > 0 && m.w2 > 0 && m.w3 > 0 && m.w4 > 0)) {
+        g_err = "bad Fig. 3 parameters"; return nullptr;
+      }
+      return new Smc<Fig3Model>(m, N, seed);
+    }
+    case K_STACKF: {
+      StackfModel m;
+      for (uint64_t i = 0; i < data_len; ++i) m.y.push_back(data[i]);
+      m.p0 = P(0, 2.0); m.prec = P(1, 2.0); m.sigma = P(2, 0.5); m.cap = (int)P(3, 768.0);
+      if (!(m.p0 > 0 && m.prec > 0 && m.sigma > 0) || m.cap < 48 || m.cap % 16 || m.cap > 65536) {
+        g_err = "bad STACKF parameters"; return nullptr;
+      }
+      return new Smc<StackfModel>(m, N, seed);
     }
     case K_CONSTW: {
       ConstwModel m; m.logw = P(0, std::log(3.0)); m.K = (int)P(1, 1.0);

@@ -25,7 +25,7 @@ _lib = C.CDLL(_LIB_PATH, mode=C.RTLD_GLOBAL)
 
 # ---- enums (include/smc.h) --------------------------------------------------
 OK, EINVAL, ECUDA, ENCCL, EREJECTED, ENAN, EOVERFLOW, ESTATE = range(8)
-CRBD, CLADS2, SEIR, GEOMETRIC, SSM, CONSTW, RESAMPLE_BENCH = 1, 2, 3, 10, 11, 12, 20
+CRBD, CLADS2, SEIR, GEOMETRIC, SSM, CONSTW, FIG3, STACKF, RESAMPLE_BENCH = 1, 2, 3, 10, 11, 12, 13, 14, 20
 FLAG_STRICT = 1
 FLAG_LINEAGE_RNG = 2
 FLAG_ANALYTIC_UNDETECTED = 4
@@ -39,6 +39,7 @@ FIELDS = {
     GEOMETRIC: ["pc", "n"],
     SSM: ["pc", "t", "x"],
     CONSTW: ["pc", "k"],
+    FIG3: ["pc", "n", "x"],
 }
 
 
@@ -191,6 +192,18 @@ class Model:
     @staticmethod
     def geometric(p=0.5, w=1.5, flags=0):
         return Model(GEOMETRIC, None, (p, w), flags=flags)
+
+    @staticmethod
+    def fig3(p_loop=0.5, p3=0.3, w1=2.0, w2=1.2, w3=1.2, w4=0.5, flags=0):
+        """The PCFG of Fig. 3(a) (R-23)."""
+        return Model(FIG3, None, (p_loop, p3, w1, w2, w3, w4), flags=flags)
+
+    @staticmethod
+    def stackf(y, params=(2.0, 2.0, 0.5, 768.0), flags=0):
+        """The recursive function of Fig. 5 compiled with a PSTATE byte stack
+        (P:905-925; DESIGN.md R-24): y = observation per recursion depth;
+        params (p0, p_rec, sigma, stack bytes)."""
+        return Model(STACKF, np.asarray(y, dtype=np.float64), params, flags=flags)
 
     @staticmethod
     def constw(logw=float(np.log(3.0)), K=1, flags=0):

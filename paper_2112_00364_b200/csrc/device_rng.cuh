@@ -71,7 +71,7 @@ __device__ __forceinline__ double d_normal(Rng& r, double mu, double sigma) {
   const double u1 = r.uniform();
   const double u2 = r.uniform();
   const double rad = sqrt(-2.0 * log(u1));
-  const double c = cos(kTwoPi * u2);
+  const double c = cospi(2.0 * u2);          // cos(2 pi u2) without a 2 pi range reduction
   return mu + sigma * (rad * c);
 }
 __device__ __noinline__ double d_gamma_mt(Rng& r, double k, double theta) {   // k > 1, Marsaglia-Tsang

@@ -314,6 +314,27 @@ int setup_model(smc_ctx* h, const smc_model* m) {
       h->mc.p[0] = P(0, 0.5); h->mc.p[1] = P(1, 1.5);
       h->planes = Geometric::kPlanes;
       break;
+    case SMC_FIG3: {
+      const double pl = P(0, 0.5), p3 = P(1, 0.3), w1 = P(2, 2.0), w2 = P(3, 1.2), w3 = P(4, 1.2),
+                   w4 = P(5, 0.5);
+      if (!(pl >= 0 && p3 >= 0 && pl + p3 <= 1 && w1 > 0 && w2 > 0 && w3 > 0 && w4 > 0))
+        return fail(h, SMC_EINVAL, "bad Fig. 3 parameters");
+      h->mc.p[0] = pl; h->mc.p[1] = p3;
+      h->mc.p[6] = std::log(w1); h->mc.p[7] = std::log(w2); h->mc.p[8] = std::log(w3);
+      h->mc.p[9] = std::log(w4);
+      h->planes = Fig3::kPlanes;
+      break;
+    }
+    case SMC_STACKF: {
+      if (m->data && m->data_len) h->h_table.assign(m->data, m->data + m->data_len);
+      h->mc.n = (int)m->data_len;
+      const double p0 = P(0, 2.0), prec = P(1, 2.0), sg = P(2, 0.5), cap = P(3, 768.0);
+      if (!(p0 > 0 && prec > 0 && sg > 0) || cap < 48 || cap > 65536 || std::fmod(cap, 16.0) != 0.0)
+        return fail(h, SMC_EINVAL, "bad STACKF parameters (cap: multiple of 16 in [48, 65536])");
+      h->mc.p[0] = p0; h->mc.p[1] = prec; h->mc.p[2] = sg; h->mc.p[3] = cap;
+      h->planes = 1 + (int)cap / 16;
+      break;
+    }
     case SMC_SSM:
       if (!m->data || m->data_len == 0) return fail(h, SMC_EINVAL, "SSM needs observations");
       h->h_table.assign(m->data, m->data + m->data_len);
@@ -663,6 +684,8 @@ void launch_propagate(smc_ctx* h, Shard& s, int cur) {
     case SMC_CLADS2: launch_prop<Clads2>(h, s, cur); break;
     case SMC_SEIR: launch_prop<Seir>(h, s, cur); break;
     case SMC_GEOMETRIC: launch_prop<Geometric>(h, s, cur); break;
+    case SMC_FIG3: launch_prop<Fig3>(h, s, cur); break;
+    case SMC_STACKF: launch_prop<Stackf>(h, s, cur); break;
     case SMC_SSM: launch_prop<Ssm>(h, s, cur); break;
     case SMC_CONSTW: launch_prop<Constw>(h, s, cur); break;
     default: break;
@@ -698,6 +721,9 @@ ResArgs res_args(smc_ctx* h, Shard& s, const double* lw, const uint4* src, int d
   a.stk0 = a.stk_n = a.stk_per = a.sp_word = 0;
   if (h->kind == SMC_CLADS2 && h->stack_prefix) {   // R-22: pending-rate stack, planes 2..4, sp = P5.z
     a.stk0 = 2; a.stk_n = 3; a.stk_per = 2; a.sp_word = 22;
+  }
+  if (h->kind == SMC_STACKF && h->stack_prefix) {   // R-24: byte stack, planes 1.., sp (bytes) = P0.y
+    a.stk0 = 1; a.stk_n = h->planes - 1; a.stk_per = 16; a.sp_word = 1;
   }
   return a;
 }
@@ -899,8 +925,10 @@ int check_ready(smc_ctx* h) {
 }
 
 // Decoded observable state.
-int nfields_of(int kind) {
+int nfields_of(int kind, int planes = 0) {
   switch (kind) {
+    case SMC_STACKF: return 3 + 6 * (((planes - 1) * 16) / 48);
+    case SMC_FIG3: return 3;
     case SMC_CRBD: return 4;
     case SMC_CLADS2: return 13;
     case SMC_SEIR: return 15;
@@ -910,7 +938,7 @@ int nfields_of(int kind) {
     default: return 0;
   }
 }
-void decode(int kind, const uint32_t* w, double* f) {
+void decode(int kind, const uint32_t* w, double* f, int planes = 0) {
   // w: the particle's planes concatenated (4 words per plane)
   auto d = [&](int word) { double x; std::memcpy(&x, w + word, 8); return x; };
   auto i = [&](int word) { return (double)(int32_t)w[word]; };
@@ -928,6 +956,21 @@ void decode(int kind, const uint32_t* w, double* f) {
       for (int k = 0; k < 3; ++k) f[12 + k] = i(16 + k);
       break;
     case SMC_GEOMETRIC: f[0] = i(0); f[1] = i(1); break;
+    case SMC_FIG3: f[0] = i(0); f[1] = i(1); f[2] = i(2); break;
+    case SMC_STACKF: {   // stack bytes at or above sp are not state (R-22/R-24): 0
+      f[0] = i(0); f[1] = i(1); f[2] = d(2);
+      const int sp = (int)w[1], nfr = ((planes - 1) * 16) / 48;
+      for (int j = 0; j < nfr; ++j) {
+        double* g = f + 3 + 6 * j;
+        const int b = 4 + 12 * j;   // first word of frame j (stack starts at plane 1 = word 4)
+        if ((j + 1) * 48 <= sp) {
+          g[0] = i(b); g[1] = i(b + 1); g[2] = d(b + 2); g[3] = d(b + 4); g[4] = d(b + 6); g[5] = d(b + 8);
+        } else {
+          for (int k = 0; k < 6; ++k) g[k] = 0.0;
+        }
+      }
+      break;
+    }
     case SMC_SSM: f[0] = i(2); f[1] = i(3); f[2] = d(0); break;
     case SMC_CONSTW: f[0] = i(0); f[1] = i(1); break;
   }
@@ -1133,7 +1176,7 @@ int smc_set_stream(smc_handle h, void* s) {
 
 int smc_set_data(smc_handle h, const double* data, uint64_t data_len) {
   if (!h) return fail(h, SMC_EINVAL, "NULL handle");
-  if (h->kind == SMC_RESAMPLE_BENCH || h->kind == SMC_GEOMETRIC || h->kind == SMC_CONSTW)
+  if (h->kind == SMC_RESAMPLE_BENCH || h->kind == SMC_GEOMETRIC || h->kind == SMC_CONSTW || h->kind == SMC_FIG3)
     return fail(h, SMC_ESTATE, "model has no data");
   // rebuild the device table exactly as setup_model does, same shape required
   smc_model m{};
@@ -1274,7 +1317,7 @@ double smc_log_z(smc_handle h) {
   return h->h_ctrl->logz;
 }
 
-int smc_nfields(smc_handle h) { return h ? nfields_of(h->kind) : 0; }
+int smc_nfields(smc_handle h) { return h ? nfields_of(h->kind, h->planes) : 0; }
 
 int smc_ancestors(smc_handle h, uint32_t* out, uint64_t n) {
   if (!h || !out || n != h->n_per * h->shards.size()) return fail(h, SMC_EINVAL, "bad output size");
@@ -1316,7 +1359,7 @@ int smc_state(smc_handle h, void* out, uint64_t bytes) {
 
 int smc_fields(smc_handle h, double* out, uint64_t n_doubles) {
   if (!h) return fail(h, SMC_EINVAL, "NULL handle");
-  const int F = nfields_of(h->kind);
+  const int F = nfields_of(h->kind, h->planes);
   const uint64_t nl = h->n_per * h->shards.size();
   if (!F || !out || n_doubles != nl * F) return fail(h, SMC_EINVAL, "bad output size");
   const uint64_t per = (uint64_t)h->planes * 16 * h->n_per;
@@ -1329,7 +1372,7 @@ int smc_fields(smc_handle h, double* out, uint64_t n_doubles) {
     for (uint64_t k = 0; k < h->n_per; ++k) {
       for (int p = 0; p < h->planes; ++p)
         for (int q = 0; q < 4; ++q) w[4 * p + q] = raw[4 * (p * h->n_per + k) + q];
-      decode(h->kind, w.data(), out + (si * h->n_per + k) * F);
+      decode(h->kind, w.data(), out + (si * h->n_per + k) * F, h->planes);
     }
   }
   return SMC_OK;

@@ -443,6 +443,11 @@ __device__ __forceinline__ int stack_skip_lo(const ResArgs& a, const uint4* plan
 __device__ __forceinline__ bool copy_plane(const ResArgs& a, int p, int skip_lo) {
   return p < skip_lo || p >= a.stk0 + a.stk_n;
 }
+// next plane to copy after p (run-time plane loops skip the planes beyond the
+// stack pointer in one step)
+__device__ __forceinline__ int next_plane(const ResArgs& a, int p, int skip_lo) {
+  return p + 1 == skip_lo ? max(p + 1, a.stk0 + a.stk_n) : p + 1;
+}
 
 struct Global {
   double m;
@@ -680,7 +685,7 @@ __global__ void __launch_bounds__(kThreads, 4) anc_gather_kernel(ResArgs a) {
     const int np = P > 0 ? P : a.planes;
     for (int k = threadIdx.x; k < cnt; k += kThreads) {
       const int lo = stack_skip_lo(a, a.src_planes, base + k);
-      for (int p = 0; p < np; ++p)
+      for (int p = 0; p < np; p = next_plane(a, p, lo))
         if (copy_plane(a, p, lo))
           dst[(unsigned long long)p * a.n_local + base + k] =
               __ldg(a.src_planes + (unsigned long long)p * a.n_local + base + k);
@@ -776,7 +781,7 @@ __global__ void __launch_bounds__(kThreads, 4) anc_gather_kernel(ResArgs a) {
       for (int p = 0; p < (P > 0 ? P : 1); ++p)
         if (copy_plane(a, p, skip)) dst[(unsigned long long)p * a.n_local + dl] = v[p];
     } else {
-      for (int p = 0; p < a.planes; ++p)
+      for (int p = 0; p < a.planes; p = next_plane(a, p, skip))
         if (copy_plane(a, p, skip))
           dst[(unsigned long long)p * a.n_local + dl] = __ldg(a.src_planes + (unsigned long long)p * a.n_local + src);
     }
@@ -998,7 +1003,7 @@ __global__ void __launch_bounds__(kThreads) fill_holes_kernel(ResArgs a) {
       for (int p = 0; p < (P > 0 ? P : 1); ++p)
         if (copy_plane(a, p, lo)) pl[(unsigned long long)p * a.n_local + dst] = v[p];
     } else {
-      for (int p = 0; p < np; ++p)
+      for (int p = 0; p < np; p = next_plane(a, p, lo))
         if (copy_plane(a, p, lo))
           pl[(unsigned long long)p * a.n_local + dst] = __ldg(pl + (unsigned long long)p * a.n_local + src);
     }
@@ -1216,7 +1221,7 @@ __device__ __forceinline__ void copy_particle(const ResArgs& a, uint4* dst, unsi
     for (int p = 0; p < (P > 0 ? P : 1); ++p)
       if (copy_plane(a, p, skip)) dst[(unsigned long long)p * a.n_local + slot] = v[p];
   } else {
-    for (int p = 0; p < a.planes; ++p)
+    for (int p = 0; p < a.planes; p = next_plane(a, p, skip))
       if (copy_plane(a, p, skip))
         dst[(unsigned long long)p * a.n_local + slot] = __ldg(a.src_planes + (unsigned long long)p * a.n_local + src);
   }

@@ -78,7 +78,7 @@ struct NodeOut {
 enum { NODE_LEAF = 0, NODE_DETECTED = 1, NODE_BIRTH = 2, NODE_GUARD = 3 };
 
 // Per-owner constants kept in shared memory during phase 2.
-struct OwnerCrbd { double tot, pb; };
+struct OwnerCrbd { double inv_tot, pb; };
 struct OwnerClads2 { double eps, alpha, sigma, pb; };
 
 // ---------------------------------------------------------------------------
@@ -117,8 +117,9 @@ struct CrbdLR {
     const bool internal = __ldg(b + 2) != 0.0;
     lw = lw + (-s.mu * (tp - tc));
     lw = lw + (internal ? log(s.lambda) : log(rho));
-    ow.tot = s.lambda + s.mu;           // before any push: phase-1 DFS reads them
-    ow.pb = s.lambda / ow.tot;
+    const double tot = s.lambda + s.mu;   // before any push: phase-2 lanes read them
+    ow.inv_tot = 1.0 / tot;
+    ow.pb = s.lambda / tot;
     double t = tp;
     K = 0;
     for (;;) {
@@ -137,7 +138,7 @@ struct CrbdLR {
                              uint32_t t, unsigned long long seed, double rho, NodeOut& out) {
     const uint4 B = side_block(seed, id, n, t, kTagNode);
     const double u0 = hq(B.x, B.y), u1 = hq(B.z, B.w);
-    const double d = -log(u0) / ow.tot;
+    const double d = -log(u0) * ow.inv_tot;   // Exp(lambda + mu)
     if (d > s) return u1 < rho ? NODE_DETECTED : NODE_LEAF;
     if (!(u1 < ow.pb)) return NODE_LEAF;                       // death
     const uint4 Cb = side_block(seed, id, n, t, kTagChild);
@@ -237,8 +238,9 @@ struct Clads2LR {
     if (!(u1 < ow.pb)) return NODE_LEAF;
     const uint4 Z = side_block(seed, id, n, t, kTagZ);
     const double rad = sqrt(-2.0 * log(hq(Z.x, Z.y)));
-    const double th = kTwoPi * hq(Z.z, Z.w);
-    const double za = rad * cos(th), zb = rad * sin(th);
+    double sn, cs;
+    sincospi(2.0 * hq(Z.z, Z.w), &sn, &cs);      // Box-Muller pair at angle 2 pi u
+    const double za = rad * cs, zb = rad * sn;
     out.la = ow.alpha * lam * exp(ow.sigma * za);
     out.lb = ow.alpha * lam * exp(ow.sigma * zb);
     if (Clads2::bad_rate(out.la) || Clads2::bad_rate(out.lb)) return NODE_GUARD;   // rate guard

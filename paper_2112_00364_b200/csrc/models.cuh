@@ -428,6 +428,154 @@ struct Seir {
 };
 
 // ============================================================================
+// The PCFG of Fig. 3(a): blocks b0..b4, PC
+// dispatch by a switch; checkpoints on the figure's regular arrows (b0 -> b1,
+// b3 -> b2, b4 -> b_stop), jumps on the open ones (b1 -> b2, b2 -> b2 | b3 |
+// b4).  Params p_loop, p3, w1, w2, w3, w4 (as log weights in C.p[6..9]).
+// Plane P0 {pc, n (b3 visits), x (b2 self-loops), 0}.
+// ============================================================================
+struct Fig3 {
+  static constexpr int kPlanes = 1;
+  static constexpr int kMinBlocks = 4;
+  static constexpr bool kOneWave = false;  // uneven work (geometric loops): block scheduler balances
+  struct State { int pc, n, x; };
+  __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
+    const uint4 v = ldp(P, st, 0, i); s.pc = (int)v.x; s.n = (int)v.y; s.x = (int)v.z;
+  }
+  __device__ static void store(const State& s, uint4* P, unsigned long long st, unsigned long long i) {
+    stp(P, st, 0, i, make_uint4((uint32_t)s.pc, (uint32_t)s.n, (uint32_t)s.x, 0u));
+  }
+  __device__ static int pc(const State& s) { return s.pc; }
+  __device__ static bool step(State& s, double& lw, Rng& r, const ModelConst& C, Diag&) {
+    switch (s.pc) {
+      case 0:                                          // b0 -> b1 (checkpoint)
+        s.n = 0; s.x = 0; s.pc = 1;
+        return true;
+      case 1:                                          // b1: weight(w1) -> b2
+        lw = lw + C.p[6]; s.pc = 2;
+        return false;
+      case 2: {                                        // b2 -> b2 | b3 | b4
+        const double u = d_uniform(r, 0.0, 1.0);
+        if (u < C.p[0]) { s.x = s.x + 1; lw = lw + C.p[7]; s.pc = 2; }
+        else if (u < C.p[0] + C.p[1]) s.pc = 3;
+        else s.pc = 4;
+        return false;
+      }
+      case 3:                                          // b3: weight(w3) -> b2 (checkpoint)
+        s.n = s.n + 1; lw = lw + C.p[8]; s.pc = 2;
+        return true;
+      default:                                         // b4: weight(w4) -> b_stop (checkpoint)
+        lw = lw + C.p[9]; s.pc = kStop;
+        return true;
+    }
+  }
+};
+
+// ============================================================================
+// STACKF (§R-24): the recursive function of Fig. 5 compiled to
+// blocks 1-4 of Fig. 5(c) with a PSTATE byte stack and stack pointer
+// (P:905-925).  Table y[D] (observation per recursion depth); params p0,
+// p_rec, sigma, cap (stack bytes).  Planes: P0 {pc, sp (bytes), result f64};
+// P1 .. P(cap/16) the stack, 16 bytes per plane (SoA like every plane): frame
+// j (STACK_f, 48 bytes) = planes 1+3j {ra, retValLoc, p}, 2+3j {s1, s3},
+// 3+3j {s4, 0}.  The blocks read and write frame fields where they touch
+// them (the stack never passes through registers); resampling copies the
+// header plane and only the planes below the stack pointer (R-22).
+// ============================================================================
+struct Stackf {
+  static constexpr int kPlanes = 0;        // 1 + cap/16, set at create
+  static constexpr int kMinBlocks = 4;
+  static constexpr bool kOneWave = false;  // uneven work (recursion depths): block scheduler balances
+  static constexpr int kFrame = 48, kRaStop = -1;
+  struct State { int pc, sp; double result; uint4* P; unsigned long long st, i; };
+  __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
+    const uint4 v = ldp(P, st, 0, i);
+    s.pc = (int)v.x; s.sp = (int)v.y; s.result = hi_d(v);
+    s.P = const_cast<uint4*>(P); s.st = st; s.i = i;
+  }
+  __device__ static void store(const State& s, uint4* P, unsigned long long st, unsigned long long i) {
+    const unsigned long long rb = __double_as_longlong(s.result);
+    stp(P, st, 0, i, make_uint4((uint32_t)s.pc, (uint32_t)s.sp, (uint32_t)rb, (uint32_t)(rb >> 32)));
+  }
+  __device__ static int pc(const State& s) { return s.pc; }
+  // the stack plane holding byte offset `off`
+  __device__ static uint4* plane(const State& s, int off) {
+    return s.P + (unsigned long long)(1 + off / 16) * s.st + s.i;
+  }
+  __device__ static bool call(State& s, int ra, int rv, double p, int cap) {
+    if (s.sp + kFrame > cap) return false;
+    const unsigned long long pb = __double_as_longlong(p);
+    *plane(s, s.sp) = make_uint4((uint32_t)ra, (uint32_t)rv, (uint32_t)pb, (uint32_t)(pb >> 32));
+    *plane(s, s.sp + 16) = make_uint4(0u, 0u, 0u, 0u);
+    *plane(s, s.sp + 32) = make_uint4(0u, 0u, 0u, 0u);
+    s.sp = s.sp + kFrame;
+    return true;
+  }
+  __device__ static bool step(State& s, double& lw, Rng& r, const ModelConst& C, Diag& dg) {
+    const int cap = (int)C.p[3];
+    const int top = s.sp - kFrame;                       // current frame (sf)
+    switch (s.pc) {
+      case 0:                                            // main: f(p0) into the result slot
+        s.sp = 0; s.result = 0.0;
+        if (!call(s, kRaStop, -1, C.p[0], cap)) { ++dg.overflow; lw = -INFINITY; s.pc = kStop; return true; }
+        s.pc = 1;
+        return false;
+      case 1: {                                          // block 1: s1 = assume Gamma p p; resample
+        const uint4 a = *plane(s, top);
+        const double p = hi_d(a);
+        const uint4 b = *plane(s, top + 16);
+        const double s1 = d_gamma(r, p, 1.0 / p);
+        const unsigned long long x = __double_as_longlong(s1);
+        *plane(s, top + 16) = make_uint4((uint32_t)x, (uint32_t)(x >> 32), b.z, b.w);
+        s.pc = 2;
+        return true;
+      }
+      case 2: {                                          // block 2: observe, branch, call
+        const uint4 b = *plane(s, top + 16);
+        const double s1 = lo_d(b);
+        const int d = s.sp / kFrame - 1;
+        if (d < C.n) lw = lw + d_normal_logpdf(__ldg(C.table + d), s1, C.p[2]);
+        if (s1 >= 1.0) {                                 // s4 = f(p_rec)
+          if (!call(s, 3, top + 32, C.p[1], cap)) { ++dg.overflow; lw = -INFINITY; s.pc = kStop; return true; }
+          s.pc = 1;
+        } else {                                         // s3 = 8
+          const unsigned long long x = __double_as_longlong(8.0);
+          *plane(s, top + 16) = make_uint4(b.x, b.y, (uint32_t)x, (uint32_t)(x >> 32));
+          s.pc = 4;
+        }
+        return false;
+      }
+      case 3: {                                          // block 3: s3 = s4 + s4
+        const uint4 b = *plane(s, top + 16);
+        const double s4 = lo_d(*plane(s, top + 32));
+        const unsigned long long x = __double_as_longlong(s4 + s4);
+        *plane(s, top + 16) = make_uint4(b.x, b.y, (uint32_t)x, (uint32_t)(x >> 32));
+        s.pc = 4;
+        return false;
+      }
+      default: {                                         // block 4: return s3 * s3
+        const uint4 a = *plane(s, top);
+        const double s3 = hi_d(*plane(s, top + 16));
+        const double t = s3 * s3;
+        const int ra = (int)a.x, rv = (int)a.y;
+        if (rv < 0) {
+          s.result = t;
+        } else {                                         // 8 bytes at retValLoc of the caller's frame
+          uint4 w = *plane(s, rv);
+          const unsigned long long x = __double_as_longlong(t);
+          if ((rv & 15) == 0) { w.x = (uint32_t)x; w.y = (uint32_t)(x >> 32); }
+          else { w.z = (uint32_t)x; w.w = (uint32_t)(x >> 32); }
+          *plane(s, rv) = w;
+        }
+        s.sp = s.sp - kFrame;
+        s.pc = ra == kRaStop ? kStop : ra;
+        return false;
+      }
+    }
+  }
+};
+
+// ============================================================================
 // Weighted geometric, Fig. 2(a).  Params p, w.  Plane P0 {pc, n, 0, 0}.
 // ============================================================================
 struct Geometric {

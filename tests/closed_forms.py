@@ -383,3 +383,83 @@ def clads2_cherry_forward(T, lam0, alpha, sigma, eps, rho, n, seed):
     px, py = x.mean(), y.mean()
     se = math.sqrt(py * py * x.var(ddof=1) / n + px * px * y.var(ddof=1) / n)
     return px * py, se
+
+
+# --------------------------------------------------------------------------
+# The PCFG of Fig. 3(a) (R-23): b1 weights w1; every visit of b2
+# draws one of {self-loop (p_loop, weight w2), b3 (p3, weight w3, back to b2),
+# b4 (p4 = 1 - p_loop - p3, weight w4, stop)}.  Summing over all paths:
+#   Z = w1 * sum_k (w3 B3)^k * w4 B4,   B3 = p3 / (1 - p_loop w2),
+#   B4 = p4 / (1 - p_loop w2)   (the self-loops of one b2 visit sum to
+#   1 / (1 - p_loop w2)),  i.e.  Z = w1 w4 B4 / (1 - w3 B3)  when w3 B3 < 1.
+# The posterior of n (visits of b3) is geometric: P(n) = (1 - r) r^n, r = w3 B3.
+def fig3_z(p_loop, p3, w1, w2, w3, w4):
+    b3 = p3 / (1.0 - p_loop * w2)
+    b4 = (1.0 - p_loop - p3) / (1.0 - p_loop * w2)
+    return w1 * w4 * b4 / (1.0 - w3 * b3)
+
+
+def fig3_z_paths(p_loop, p3, w1, w2, w3, w4, steps=20000):
+    """The same Z by propagating the prior-weighted mass of the program's paths
+    through b2, one b2 decision per step (no series summed in closed form)."""
+    p4 = 1.0 - p_loop - p3
+    at_b2, z = w1, 0.0
+    for _ in range(steps):
+        z += at_b2 * p4 * w4
+        at_b2 = at_b2 * (p_loop * w2 + p3 * w3)
+    return z
+
+
+def fig3_posterior_n(p_loop, p3, w3, w2, nmax):
+    r = w3 * p3 / (1.0 - p_loop * w2)
+    return np.array([(1.0 - r) * r ** n for n in range(nmax + 1)])
+
+
+# --------------------------------------------------------------------------
+# STACKF (DESIGN.md R-24): the recursive function of Fig. 5 made to terminate.
+# f(p) at depth d: s ~ Gamma(p, 1/p); weight N(y_d; s, sigma) (d < |y|);
+# recurse with p_rec iff s >= 1.  With D = cap // 48 frames a call from depth
+# d needs frame d + 1 (allowed iff d + 2 <= D; otherwise the particle dies).
+#   V_d = int_0^1 g_d(s) l_d(s) ds + [d + 2 <= D] V_{d+1} int_1^inf g_d(s) l_d(s) ds
+#   Z = V_0,  g_d = Gamma(p_d, 1/p_d) density, p_0 = p0, p_d = p_rec (d >= 1).
+def stackf_z(y, p0, prec, sigma, cap):
+    from scipy import integrate, stats
+    D = cap // 48
+
+    def parts(d):
+        p = p0 if d == 0 else prec
+        g = stats.gamma(a=p, scale=1.0 / p)
+        if d < len(y):
+            f = lambda s: g.pdf(s) * stats.norm.pdf(y[d], loc=s, scale=sigma)   # noqa: E731
+        else:
+            f = g.pdf
+        lo = integrate.quad(f, 0.0, 1.0, epsabs=0, epsrel=1e-12, limit=200)[0]
+        hi = integrate.quad(f, 1.0, np.inf, epsabs=0, epsrel=1e-12, limit=200)[0]
+        return lo, hi
+
+    V = 0.0
+    for d in range(D - 1, -1, -1):
+        lo, hi = parts(d)
+        V = lo + (hi * V if d + 2 <= D else 0.0)
+    return V
+
+
+def stackf_forward(y, p0, prec, sigma, cap, n, seed):
+    """Brute-force forward simulation of the same program (numpy draws):
+    returns (mean weight, its standard error) -- E[weight] = Z."""
+    from scipy import stats
+    g = np.random.Generator(np.random.PCG64(seed))
+    D = cap // 48
+    w = np.ones(n)
+    alive = np.ones(n, dtype=bool)          # still recursing
+    for d in range(D):
+        p = p0 if d == 0 else prec
+        s = g.gamma(p, 1.0 / p, size=n)
+        if d < len(y):
+            w = np.where(alive, w * stats.norm.pdf(y[d], loc=s, scale=sigma), w)
+        rec = alive & (s >= 1.0)
+        if d + 2 > D:
+            w = np.where(rec, 0.0, w)       # the call would overflow the stack
+            rec[:] = False
+        alive = rec
+    return w.mean(), w.std(ddof=1) / np.sqrt(n)

@@ -56,6 +56,9 @@ CASES = [
     ("ssm_peaked", "SSM", None, [0.0, 100.0, 2.0, 1.0, 1e-4], None, None, 200_000),
     ("geometric_ess", "GEOMETRIC", None, None, None, (1, 2), 2049),
     ("constw", "CONSTW", None, None, None, None, 1),
+    ("fig3", "FIG3", None, "FIG3_PARAMS", None, None, 30_001),
+    ("stackf", "STACKF", None, "STACKF_PARAMS", None, None, 30_001),
+    ("stackf_ess", "STACKF", None, "STACKF_PARAMS", None, (1, 2), 9_999),
 ]
 
 
@@ -67,6 +70,8 @@ def case_args(smc, name, kind, data, params, flag, ess, N):
         d = inputs.seir_series()
     elif kind == "SSM":
         d = inputs.ssm_series(50)
+    elif kind == "STACKF":
+        d = inputs.stackf_series()
     else:
         d = None
     p = (getattr(inputs, params) if isinstance(params, str) else params) if params else None

@@ -124,10 +124,14 @@ def run_pair_inplace(smc, kind, data, params, N, seed, ess=None, per_epoch=True,
     (oracle.GEOMETRIC, None, inputs.GEOMETRIC_PARAMS, 3001, None),
     (oracle.SSM, "ssm", inputs.SSM_PARAMS, 2000, (3, 4)),
     (oracle.CONSTW, None, inputs.CONSTW_PARAMS, 10, None),
+    (oracle.FIG3, None, inputs.FIG3_PARAMS, 4001, None),
+    (oracle.STACKF, "stackf", inputs.STACKF_PARAMS, 4001, None),
+    (oracle.STACKF, "stackf", inputs.STACKF_PARAMS, 4001, (1, 2)),
 ])
 def test_inplace_smc_parity(smc, kind, data, params, N, ess):
     data = {"tree5": lambda: inputs.tree("tree5"), "tree90": lambda: inputs.tree("tree90"),
-            "seir": inputs.seir_series, "ssm": lambda: inputs.ssm_series(10)}.get(data, lambda: data)()
+            "seir": inputs.seir_series, "ssm": lambda: inputs.ssm_series(10),
+            "stackf": inputs.stackf_series}.get(data, lambda: data)()
     run_pair_inplace(smc, kind, data, params, N, 11, ess=ess, per_epoch=kind != oracle.SEIR)
 
 

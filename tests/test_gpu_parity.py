@@ -152,6 +152,26 @@ def test_ssm(smc):
     run_pair(smc, oracle.SSM, inputs.ssm_series(50), inputs.SSM_PARAMS, 3000, 5)
 
 
+@pytest.mark.parametrize("N", [1, 31, 3001, 100_003])
+def test_fig3_pcfg(smc, N):
+    # the PCFG of Fig. 3(a): PC dispatch over five blocks, jumps and
+    # checkpoints, particles stopping at different epochs (DESIGN R-23)
+    run_pair(smc, oracle.FIG3, None, inputs.FIG3_PARAMS, N, 12)
+
+
+def test_fig3_pcfg_other_params(smc):
+    run_pair(smc, oracle.FIG3, None, [0.2, 0.5, 1.0, 2.0, 1.1, 3.0], 5000, 13)
+
+
+@pytest.mark.parametrize("N,cap", [(1, 768), (2049, 768), (100_003, 768), (5000, 96), (3000, 4096)])
+def test_stackf_pstate_stack(smc, N, cap):
+    # the compiled recursion of Fig. 5(c) with a byte-array PSTATE stack
+    # (DESIGN R-24): frames and return values element by element; resampling
+    # copies only the stack planes below each ancestor's stack pointer, so
+    # stale bytes above it must never reach the output (fields report them 0)
+    run_pair(smc, oracle.STACKF, inputs.stackf_series(), inputs.STACKF_PARAMS[:3] + [cap], N, 14)
+
+
 CRBD_K = pytest.mark.parametrize("ck", [oracle.CRBD, oracle.CRBD_LR, oracle.CRBD_AE],
                                  ids=["seq", "lineage", "analytic"])
 CLADS_K = pytest.mark.parametrize("ck", [oracle.CLADS2, oracle.CLADS2_LR], ids=["seq", "lineage"])
@@ -264,6 +284,8 @@ def test_seir_full_size_prefix(smc):
     (oracle.CRBD_AE, "tree90", inputs.CRBD_PARAMS, 5000),
     (oracle.CLADS2_LR, "tree90", inputs.CLADS2_PARAMS, 3000),
     (oracle.GEOMETRIC, None, inputs.GEOMETRIC_PARAMS, 3001),     # particles stop at different epochs
+    (oracle.FIG3, None, None, 4001),                             # Fig. 3(a): five blocks, PC dispatch
+    (oracle.STACKF, "stackf", None, 3001),                       # Fig. 5(c): PSTATE byte stack
     (oracle.SEIR, "seir", None, 1500),
     (oracle.CONSTW, None, inputs.CONSTW_PARAMS, 10),
 ])
@@ -272,6 +294,8 @@ def test_graph_run_matches_oracle(smc, kind, data, params, N):
         data = inputs.tree("tree90")
     elif data == "seir":
         data = inputs.seir_series()
+    elif data == "stackf":
+        data = inputs.stackf_series()
     g, o = both(smc, kind, data, params, N, 31)
     rg = g.run_status()          # one graph launch (WHILE node)
     ro = o.run()
