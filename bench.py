@@ -51,6 +51,10 @@ WORKLOADS = {
                  desc="the PCFG of Fig. 3(a): five blocks with jumps, a self-loop and checkpoints; "
                       "particles at different blocks within an epoch and stopping at different "
                       "epochs (SURVEY f4, DESIGN R-23)"),
+    "stackf": dict(config=None, model="stackf", n=1_000_000, cap=1024,
+                   desc="the recursive function of Fig. 5(c) compiled with a 1 KiB PSTATE byte stack "
+                        "(48-byte frames) and a stack pointer; resampling copies only the stack below "
+                        "the pointer (SURVEY f2, DESIGN R-24)"),
     "resample": dict(config=4, model="resample", n=1 << 26,
                      desc="resampling step alone: LSE max + u128 scan + systematic ancestors + 64-B gather"),
 }
@@ -153,6 +157,8 @@ def model_for(smc, wl, rng="lineage", inplace=False):
         return smc.Model.ssm(inputs.ssm_series(50), inputs.SSM_PARAMS, flags=fl)
     if wl["model"] == "fig3":
         return smc.Model.fig3(*inputs.FIG3_PARAMS, flags=fl)
+    if wl["model"] == "stackf":
+        return smc.Model.stackf(inputs.stackf_series(), inputs.STACKF_PARAMS[:3] + [float(wl["cap"])], flags=fl)
     raise ValueError(wl)
 
 
@@ -165,7 +171,8 @@ def oracle_sweep_rate(wl, budget_s=15.0, n_cap=None):
     lin = getattr(oracle_sweep_rate, "rng", "lineage") == "lineage"
     kind = {"crbd": (oracle.CRBD_AE if wl.get("analytic") else oracle.CRBD_LR if lin else oracle.CRBD),
             "clads2": oracle.CLADS2_LR if lin else oracle.CLADS2, "seir": oracle.SEIR,
-            "geometric": oracle.GEOMETRIC, "ssm": oracle.SSM, "fig3": oracle.FIG3}[wl["model"]]
+            "geometric": oracle.GEOMETRIC, "ssm": oracle.SSM, "fig3": oracle.FIG3,
+            "stackf": oracle.STACKF}[wl["model"]]
     if wl["model"] in ("crbd", "clads2"):
         data = oracle.tree_blob(inputs.tree(wl["tree"]))
         params = inputs.CRBD_PARAMS if wl["model"] == "crbd" else inputs.CLADS2_PARAMS
@@ -173,6 +180,8 @@ def oracle_sweep_rate(wl, budget_s=15.0, n_cap=None):
         data, params = None, inputs.GEOMETRIC_PARAMS
     elif wl["model"] == "fig3":
         data, params = None, inputs.FIG3_PARAMS
+    elif wl["model"] == "stackf":
+        data, params = inputs.stackf_series(), inputs.STACKF_PARAMS[:3] + [float(wl["cap"])]
     elif wl["model"] == "ssm":
         data, params = inputs.ssm_series(50), inputs.SSM_PARAMS
     else:
@@ -310,6 +319,7 @@ def bench_sweeps(args, wl, smc, torch, world, rank):
     prop_ms = res_ms = 0.0
     res_bytes = 0
     n_resamples = 0
+    stack_planes = 0
     for k in range(args.steps):
         h.reset(1 + k)
         h.run()
@@ -320,8 +330,13 @@ def bench_sweeps(args, wl, smc, torch, world, rank):
         n_loc = st["n_local"]
         # algorithmic resample bytes of the sweep: per resample N*20 + S*(D + N),
         # plus the final epoch's reduce (8 B/particle)
-        res_bytes += st["resamples"] * n_loc * (20 + sb) + sb * st["distinct"] + 8 * n_loc
+        if st["stack_planes"]:
+            # stack models: the gathers copy only the planes below the stack pointer
+            res_bytes += st["resamples"] * n_loc * 20 + 16 * st["stack_planes"] * 2 + 8 * n_loc
+        else:
+            res_bytes += st["resamples"] * n_loc * (20 + sb) + sb * st["distinct"] + 8 * n_loc
         n_resamples += st["resamples"]
+        stack_planes += st["stack_planes"]
     h.set_timing(False)
     # graph body = 2 epochs x (propagate + resampling) + set_condition; the
     # resampling step is one cooperative launch when the handle uses the fused
@@ -333,6 +348,7 @@ def bench_sweeps(args, wl, smc, torch, world, rank):
     return dict(h=h, model=model, N=N, t_ms=t_ms, value=value, sweeps=sweeps_per_s, prop_ms=prop_ms,
                 res_bytes=res_bytes, resamples_per_sweep=n_resamples / args.steps,
                 res_ms=res_ms, draws=draws, guard=guard, alive_steps=alive_steps, epochs=steps_done,
+                stack_planes=stack_planes, state_bytes=st["state_bytes"],
                 launches=launches, fused=fused, clocks=clk.summary(torch.cuda.current_device()),
                 logz=float(np.mean(logzs)))
 
@@ -668,6 +684,21 @@ def sweep_line(args, name, wl, smc, torch, world, rank, pk, pk_kind, draw_peak, 
                 gpu_launches=r["launches"], clocks=r["clocks"])
     if wl["model"] == "clads2":
         line["guard_kills_per_particle_step"] = r["guard"] / max(r["alive_steps"], 1)
+    if wl["model"] == "stackf" and r["resamples_per_sweep"]:
+        # the paper's "critical optimization": bytes of state each
+        # output slot copies, with the stack-prefix copy and with the whole
+        # user-defined stack (SMC_NO_STACK_PREFIX=1, same sweeps)
+        per_slot = 16.0 * r["stack_planes"] / (r["resamples_per_sweep"] * steps * N)
+        os.environ["SMC_NO_STACK_PREFIX"] = "1"
+        try:
+            rf = bench_sweeps(sub_args, wl, smc, torch, world, rank)
+        finally:
+            os.environ.pop("SMC_NO_STACK_PREFIX", None)
+        rf["h"].close()
+        line["stack_copy"] = dict(bytes_per_slot_prefix=per_slot, bytes_per_slot_full=float(r["state_bytes"]),
+                                  resample_ms_per_sweep_prefix=r["res_ms"] / steps,
+                                  resample_ms_per_sweep_full=rf["res_ms"] / steps,
+                                  ms_per_sweep_full=rf["t_ms"] / steps)
     if with_e2e:
         e = e2e_sweeps(sub_args, wl, smc, torch, r["h"], r["model"], min(steps, 3), world)
         tot = sum_over_ranks(torch, world, r["alive_steps"] / steps)

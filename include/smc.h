@@ -154,6 +154,9 @@ typedef struct {
                                        reset (per call for smc_resample_*)                   */
   double ms_kernel[4];              /* resample-only path with timing on: CUDA-event ms of
                                        max, reduce, anc_gather, finalize (accumulated)       */
+  uint64_t stack_planes;            /* stack models (ClaDS2, STACKF): 16-byte state planes the
+                                       out-of-place gathers copied, summed since reset (the
+                                       stack prefix only, R-22/R-24)                          */
   uint64_t guard_kills;             /* ClaDS2: particle-steps set to -inf by the rate guard
                                        (R-14b; under SMC_FLAG_LINEAGE_RNG a step
                                        whose side trees both detect and break the guard may

@@ -1394,14 +1394,14 @@ int smc_stats(smc_handle h, smc_stats_t* out) {
   out->timed_epochs = h->timed_epochs;
   for (int k = 0; k < 4; ++k) out->ms_kernel[k] = h->ms_kernel[k];
   if (h->stream && cudaStreamSynchronize(h->stream) == cudaSuccess) {
-    unsigned long long alive = 0, ovf = 0, fe = ~0ull, drw = 0, roots = 0, dist = 0, grd = 0;
+    unsigned long long alive = 0, ovf = 0, fe = ~0ull, drw = 0, roots = 0, dist = 0, grd = 0, stk = 0;
     unsigned mr = 0, mn = 0;
     for (auto& s : h->shards) {
       Ctrl c;
       if (cudaMemcpy(&c, s.ctrl, sizeof(c), cudaMemcpyDeviceToHost) != cudaSuccess) break;
       alive += c.alive_steps; ovf += c.overflow; fe = std::min(fe, c.first_err); drw += c.draws;
       roots += c.side_roots; mr = std::max(mr, c.max_rounds); mn = std::max(mn, c.max_side_nodes);
-      dist += c.distinct; grd += c.guard_kills;
+      dist += c.distinct; grd += c.guard_kills; stk += c.stack_planes;
       out->epochs = c.epochs; out->resamples = c.resamples; out->done = c.done;
       if (c.status && !out->status) out->status = status_of(c);
     }
@@ -1413,6 +1413,7 @@ int smc_stats(smc_handle h, smc_stats_t* out) {
     out->max_rounds = mr;
     out->max_side_nodes = mn;
     out->guard_kills = grd;
+    out->stack_planes = stk;
     out->first_error_particle = fe == ~0ull ? -1 : (int64_t)fe;
   }
   return SMC_OK;

@@ -68,6 +68,7 @@ struct Ctrl {
   unsigned holes;                    // in-place resampling (R-21): slots without offspring
   unsigned bar_count, bar_gen;       // grid barrier of resample_fused_kernel
   unsigned long long guard_kills;    // ClaDS2 rate guard (R-14b): killed particle-steps
+  unsigned long long stack_planes;   // stack models: 16-byte planes copied by the gathers (R-22/R-24)
 };
 
 enum { ST_OK = 0, ST_REJECTED = 4, ST_NAN = 5, ST_OVERFLOW = 6 };
@@ -443,6 +444,11 @@ __device__ __forceinline__ int stack_skip_lo(const ResArgs& a, const uint4* plan
 __device__ __forceinline__ bool copy_plane(const ResArgs& a, int p, int skip_lo) {
   return p < skip_lo || p >= a.stk0 + a.stk_n;
 }
+// planes a slot copies (stack models: the planes below the stack pointer)
+__device__ __forceinline__ unsigned planes_copied(const ResArgs& a, int skip_lo) {
+  const int hi = a.stk0 + a.stk_n;
+  return (unsigned)(a.planes - (hi - min(max(skip_lo, a.stk0), hi)));
+}
 // next plane to copy after p (run-time plane loops skip the planes beyond the
 // stack pointer in one step)
 __device__ __forceinline__ int next_plane(const ResArgs& a, int p, int skip_lo) {
@@ -758,6 +764,7 @@ __global__ void __launch_bounds__(kThreads, 4) anc_gather_kernel(ResArgs a) {
   const unsigned long long j_end = heavy ? jhi : wB;
   const unsigned j_step = heavy ? kThreads : 32;
   const int s_lo = heavy ? 0 : wk0, s_hi = heavy ? kTile - 1 : wk0 + wn - 1;
+  unsigned long long stk_copied = 0;        // stack models: planes copied (bench bytes)
   for (unsigned long long j = j_first; j < j_end; j += j_step) {
     int lo = s_lo, hi = s_hi;               // first item with O_k > j
     while (lo < hi) {
@@ -772,6 +779,7 @@ __global__ void __launch_bounds__(kThreads, 4) anc_gather_kernel(ResArgs a) {
     }
     uint4* dst = a.dst_planes[dshard];
     const int skip = stack_skip_lo(a, a.src_planes, src);     // R-22: stack prefix only
+    if (a.stk_n) stk_copied += planes_copied(a, skip);
     if (P > 0) {
       uint4 v[P > 0 ? P : 1];
 #pragma unroll
@@ -786,6 +794,11 @@ __global__ void __launch_bounds__(kThreads, 4) anc_gather_kernel(ResArgs a) {
           dst[(unsigned long long)p * a.n_local + dl] = __ldg(a.src_planes + (unsigned long long)p * a.n_local + src);
     }
     a.dst_anc[dshard][dl] = (uint32_t)(a.shard_base + src);
+  }
+  if (a.stk_n) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) stk_copied += __shfl_xor_sync(0xffffffffu, stk_copied, d);
+    if ((threadIdx.x & 31) == 0 && stk_copied) atomicAdd(&a.ctrl->stack_planes, stk_copied);
   }
   if (a.world > 1) __threadfence_system();   // peer stores visible before the epoch barrier
 }
@@ -1387,6 +1400,7 @@ __global__ void __launch_bounds__(kFT, SMC_FUSED_MINB) resample_fused_kernel(Res
   // dominant weights), the whole CTA instead shares the block's slots, so a
   // single heavy particle is copied by kFT threads, not 32.
   constexpr unsigned kHeavy = 8;
+  unsigned long long stk_copied = 0;                    // stack models: planes copied (bench bytes)
   __shared__ unsigned s_heavy;
   if (threadIdx.x == 0) s_heavy = 0;
   __syncthreads();
@@ -1438,7 +1452,9 @@ __global__ void __launch_bounds__(kFT, SMC_FUSED_MINB) resample_fused_kernel(Res
           const unsigned j = j0 + 32 * u;
           if (j < wB) {
             const unsigned long long sp = base + src[u];
-            copy_particle<P>(a, dst, sp, j, stack_skip_lo(a, a.src_planes, sp));
+            const int skip = stack_skip_lo(a, a.src_planes, sp);
+            if (a.stk_n) stk_copied += planes_copied(a, skip);
+            copy_particle<P>(a, dst, sp, j, skip);
             anc[j] = (uint32_t)(a.shard_base + sp);
           }
         }
@@ -1453,13 +1469,20 @@ __global__ void __launch_bounds__(kFT, SMC_FUSED_MINB) resample_fused_kernel(Res
         if (s_O[mid] > j) hi = mid; else lo = mid + 1;
       }
       const unsigned long long src = base + lo;
-      copy_particle<P>(a, dst, src, j, stack_skip_lo(a, a.src_planes, src));
+      const int skip = stack_skip_lo(a, a.src_planes, src);
+      if (a.stk_n) stk_copied += planes_copied(a, skip);
+      copy_particle<P>(a, dst, src, j, skip);
       anc[j] = (uint32_t)(a.shard_base + src);
     }
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) distinct += __shfl_xor_sync(0xffffffffu, distinct, d);
   if (lane == 0 && distinct) atomicAdd(&c->distinct, (unsigned long long)distinct);
+  if (a.stk_n) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) stk_copied += __shfl_xor_sync(0xffffffffu, stk_copied, d);
+    if (lane == 0 && stk_copied) atomicAdd(&c->stack_planes, stk_copied);
+  }
 }
 
 }  // namespace smc

@@ -162,26 +162,54 @@ struct Clads2LR {
 #define SMC_LRW_MINB_CLADS2 4
 #endif
   static constexpr int kLRWMinBlocks = SMC_LRW_MINB_CLADS2;
-  typedef Clads2::State State;
+  // Lean state: the pending-rate stack (planes 2..4, R-22) stays in global
+  // memory; a push writes its 8-byte entry, a pop reads one, and the stack
+  // never occupies registers (12 registers and 3 plane loads/stores per
+  // particle-step less than Clads2::State; same planes, same values).
+  struct State { double sigma, alpha, eps, lam; int pc, branch, sp; uint4* P; unsigned long long st, i; };
   typedef OwnerClads2 Owner;
   static constexpr int kPlanes = Clads2::kPlanes;
   static constexpr bool kHasLam = true;
   __device__ static void load(State& s, const uint4* P, unsigned long long st, unsigned long long i) {
-    Clads2::load(s, P, st, i);
+    uint4 v = ldp(P, st, 5, i); s.pc = (int)v.x; s.branch = (int)v.y; s.sp = (int)v.z;
+    v = ldp(P, st, 0, i); s.sigma = lo_d(v); s.alpha = hi_d(v);
+    v = ldp(P, st, 1, i); s.eps = lo_d(v); s.lam = hi_d(v);
+    s.P = const_cast<uint4*>(P); s.st = st; s.i = i;
   }
   __device__ static void store(const State& s, uint4* P, unsigned long long st, unsigned long long i) {
-    Clads2::store(s, P, st, i);
+    stp(P, st, 0, i, pack_dd(s.sigma, s.alpha));
+    stp(P, st, 1, i, pack_dd(s.eps, s.lam));
+    stp(P, st, 5, i, make_uint4((uint32_t)s.pc, (uint32_t)s.branch, (uint32_t)s.sp, 0u));
   }
   __device__ static int pc(const State& s) { return s.pc; }
+  __device__ static double* pend_slot(const State& s, int k) {
+    return reinterpret_cast<double*>(s.P + (unsigned long long)(2 + (k >> 1)) * s.st + s.i) + (k & 1);
+  }
+  __device__ static void push_pend(State& s, double v) { *pend_slot(s, s.sp) = v; s.sp = s.sp + 1; }
+  __device__ static double pop_pend(State& s) { s.sp = s.sp - 1; return *pend_slot(s, s.sp); }
+  __device__ static double daughter(const State& s, double lam, double z) {
+    return s.alpha * lam * exp(s.sigma * z);
+  }
 
   template <class Push>
   __device__ static bool main_part(State& s, double& lw, Rng& r, const ModelConst& C, Owner& ow,
                                    int& K, Push push) {
     const double rho = C.p[0];
     K = 0;
-    if (s.pc == 0) {                          // INIT + root split: identical to §R-14
-      Diag dg;
-      Clads2::step(s, lw, r, C, dg);
+    if (s.pc == 0) {                          // INIT + root split: the draws of Clads2::step (§R-14)
+      const double lam0 = C.p[1] >= 0.0 ? C.p[1] : d_gamma(r, 1.0, 1.0);
+      s.sigma = C.p[2] >= 0.0 ? C.p[2] : sqrt(1.0 / d_gamma(r, 1.0, 1.0 / 0.2));
+      s.alpha = C.p[3] >= 0.0 ? C.p[3] : exp(d_normal(r, 0.0, s.sigma));
+      s.eps = C.p[4] >= 0.0 ? C.p[4] : d_uniform(r, 0.0, 1.0);
+      const double zl = d_normal(r, 0.0, 1.0);
+      const double zr = d_normal(r, 0.0, 1.0);
+      const double rl = daughter(s, lam0, zl), rr = daughter(s, lam0, zr);
+      const bool fl = C.p[5] != 0.0;
+      s.sp = 0;
+      push_pend(s, fl ? rr : rl);
+      s.lam = fl ? rl : rr;
+      s.branch = 0;
+      s.pc = 1;
     }
     ow.eps = s.eps; ow.alpha = s.alpha; ow.sigma = s.sigma;
     ow.pb = 1.0 / (1.0 + s.eps);
@@ -201,27 +229,27 @@ struct Clads2LR {
       t = t - dt;
       const double zs = d_normal(r, 0.0, 1.0);
       const double zc = d_normal(r, 0.0, 1.0);
-      const double ls = Clads2::daughter(s, s.lam, zs);
+      const double ls = daughter(s, s.lam, zs);
       if (Clads2::bad_rate(ls)) { killed = true; break; }
       push(t, ls, (unsigned)K);
       ++K;
-      s.lam = Clads2::daughter(s, s.lam, zc);
+      s.lam = daughter(s, s.lam, zc);
       if (Clads2::bad_rate(s.lam)) { killed = true; break; }
     }
     if (!killed && internal) {
       lw = lw + log(s.lam);
       const double zl = d_normal(r, 0.0, 1.0);
       const double zr = d_normal(r, 0.0, 1.0);
-      const double rl = Clads2::daughter(s, s.lam, zl), rr = Clads2::daughter(s, s.lam, zr);
+      const double rl = daughter(s, s.lam, zl), rr = daughter(s, s.lam, zr);
       if (Clads2::bad_rate(rl) || Clads2::bad_rate(rr)) {
         killed = true;
       } else {
-        Clads2::push(s, first_left ? rr : rl);
+        push_pend(s, first_left ? rr : rl);
         s.lam = first_left ? rl : rr;
       }
     } else if (!killed) {
       lw = lw + log(rho);
-      if (s.branch + 1 < C.n) s.lam = Clads2::pop(s);
+      if (s.branch + 1 < C.n) s.lam = pop_pend(s);
     }
     if (killed) lw = -INFINITY;
     s.branch = s.branch + 1;
