@@ -649,7 +649,8 @@ def sweep_line(args, name, wl, smc, torch, world, rank, pk, pk_kind, draw_peak, 
     alg_rate = (odps * r["alive_steps"] / steps / prop_s / 1e9) if odps else None
     peak = draw_peak if draw_peak else derived_peak
     prop_frac = r["prop_ms"] / max(r["prop_ms"] + r["res_ms"], 1e-9)
-    kname = ("propagate_lr_kernel" if lin else "propagate_kernel") + f"<{name}>"
+    lr_name = "propagate_lr_kernel" if os.environ.get("SMC_LR_KERNEL") == "cta" else "propagate_lrw_kernel"
+    kname = (lr_name if lin else "propagate_kernel") + f"<{name}>"
     line = dict(metric="particle-steps/s", value=r["value"], unit="particle-steps/s",
                 n_gpus=world, steps=steps, warmup=sub_args.warmup,
                 ms_per_step=r["t_ms"] / steps, higher_is_better=True, scaling="weak",

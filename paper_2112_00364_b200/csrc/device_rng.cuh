@@ -53,6 +53,38 @@ struct Rng {
     has_spare = true;
     return hq(r.x, r.y);
   }
+  // The next six uniforms of the stream, without consuming them: the three
+  // Philox blocks they need are independent (instruction-level parallelism
+  // instead of one block per dependent uniform() call).  consume(n, u), n <= 5,
+  // then advances the stream exactly as n calls of uniform() would.
+  __device__ __forceinline__ void peek6(double u[6]) const {
+    const uint4 a = philox4x32_10(make_uint4(blk, t, n, 0u), k0, k1);
+    const uint4 b = philox4x32_10(make_uint4(blk + 1u, t, n, 0u), k0, k1);
+    const uint4 c = philox4x32_10(make_uint4(blk + 2u, t, n, 0u), k0, k1);
+    const double h[6] = {hq(a.x, a.y), hq(a.z, a.w), hq(b.x, b.y), hq(b.z, b.w), hq(c.x, c.y), hq(c.z, c.w)};
+    if (has_spare) {
+      u[0] = spare;
+#pragma unroll
+      for (int k = 1; k < 6; ++k) u[k] = h[k - 1];
+    } else {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) u[k] = h[k];
+    }
+  }
+  // The next two uniforms from ONE Philox block (u[2] = the block's other half
+  // when the first came from the spare): consume(cnt <= 2, u) follows.
+  __device__ __forceinline__ void peek2(double u[3]) const {
+    const uint4 a = philox4x32_10(make_uint4(blk, t, n, 0u), k0, k1);
+    if (has_spare) { u[0] = spare; u[1] = hq(a.x, a.y); u[2] = hq(a.z, a.w); }
+    else { u[0] = hq(a.x, a.y); u[1] = hq(a.z, a.w); u[2] = 0.0; }
+  }
+  __device__ __forceinline__ void consume(int cnt, const double* u) {
+    // position of the next uniform: 2 blk - has_spare
+    const uint32_t p = 2u * blk - (has_spare ? 1u : 0u) + (uint32_t)cnt;
+    blk = (p + 1u) >> 1;
+    has_spare = (p & 1u) != 0u;
+    if (has_spare) spare = u[cnt];          // half 1 of block p >> 1 (peeked)
+  }
 };
 
 // ---- samplers (draw counts: Exp 1, Bernoulli 1, Uniform 1, Normal 2,

@@ -39,6 +39,9 @@ namespace smc {
 #ifndef SMC_LR_OPT
 #define SMC_LR_OPT 1
 #endif
+#ifndef SMC_CLADS2_SPEC_Z
+#define SMC_CLADS2_SPEC_Z 1     // ClaDS2 nodes: daughters' noise block before the event test (measured -1.3%)
+#endif
 constexpr int kLRThreads = SMC_LR_THREADS;     // threads per CTA = lanes per cooperative round
 constexpr int kOPT = SMC_LR_OPT;                 // particles (owners) per thread
 constexpr int kOwners = kLRThreads * kOPT;       // particles per batch
@@ -122,11 +125,22 @@ struct CrbdLR {
     ow.pb = s.lambda / tot;
     double t = tp;
     K = 0;
+    // hidden event times t -= Exp(lambda) until t <= t_c (the draws of d_exp,
+    // two per iteration from one Philox block, their logs side by side)
     for (;;) {
-      t = t - d_exp(r, s.lambda);
-      if (t <= tc) break;
-      push(t, 0.0, (unsigned)K);
+      double u[3];
+      r.peek2(u);
+      const double t1 = t - (-log(u[0]) / s.lambda);
+      const double e1 = -log(u[1]) / s.lambda;
+      if (t1 <= tc) { r.consume(1, u); break; }
+      push(t1, 0.0, (unsigned)K);
       ++K;
+      const double t2 = t1 - e1;
+      r.consume(2, u);
+      if (t2 <= tc) break;
+      push(t2, 0.0, (unsigned)K);
+      ++K;
+      t = t2;
     }
     s.branch = s.branch + 1;
     s.pc = (s.branch == C.n) ? kStop : 1;
@@ -220,15 +234,22 @@ struct Clads2LR {
     bool killed = Clads2::bad_rate(s.lam);
     double t = tp;
     while (!killed) {
-      const double dt = d_exp(r, s.lam);
+      // one hidden event = Exp(lam_cur), then z_side, z_cont ~ N(0, 1): the
+      // same five uniforms and formulas as d_exp + 2 d_normal (R-3, R-14),
+      // their Philox blocks and the two Box-Muller chains computed side by side
+      double u[6];
+      r.peek6(u);
+      const double dt = -log(u[0]) / s.lam;
       if (t - dt <= tc) {
+        r.consume(1, u);
         lw = lw + (-s.eps * s.lam * (t - tc));
         break;
       }
+      r.consume(5, u);
       lw = lw + (-s.eps * s.lam * dt);
       t = t - dt;
-      const double zs = d_normal(r, 0.0, 1.0);
-      const double zc = d_normal(r, 0.0, 1.0);
+      const double zs = 0.0 + 1.0 * (sqrt(-2.0 * log(u[1])) * cospi(2.0 * u[2]));
+      const double zc = 0.0 + 1.0 * (sqrt(-2.0 * log(u[3])) * cospi(2.0 * u[4]));
       const double ls = daughter(s, s.lam, zs);
       if (Clads2::bad_rate(ls)) { killed = true; break; }
       push(t, ls, (unsigned)K);
@@ -260,11 +281,16 @@ struct Clads2LR {
   __device__ static int node(double s, double lam, unsigned long long id, const Owner& ow, uint32_t n,
                              uint32_t t, unsigned long long seed, double rho, NodeOut& out) {
     const uint4 B = side_block(seed, id, n, t, kTagNode);
+#if SMC_CLADS2_SPEC_Z
+    const uint4 Z = side_block(seed, id, n, t, kTagZ);     // speculative: independent of B
+#endif
     const double u0 = hq(B.x, B.y), u1 = hq(B.z, B.w);
     const double d = -log(u0) / (lam * (1.0 + ow.eps));
     if (d > s) return u1 < rho ? NODE_DETECTED : NODE_LEAF;
     if (!(u1 < ow.pb)) return NODE_LEAF;
+#if !SMC_CLADS2_SPEC_Z
     const uint4 Z = side_block(seed, id, n, t, kTagZ);
+#endif
     const double rad = sqrt(-2.0 * log(hq(Z.x, Z.y)));
     double sn, cs;
     sincospi(2.0 * hq(Z.z, Z.w), &sn, &cs);      // Box-Muller pair at angle 2 pi u

@@ -33,6 +33,10 @@ namespace smc {
 constexpr int kWThreads = SMC_LRW_THREADS;       // CTA = kWThreads / 32 independent warps
 constexpr int kWWarps = kWThreads / 32;
 constexpr int kWSeg = 256;                       // per-owner LIFO segment (tasks)
+#ifndef SMC_LRW_WMAX
+#define SMC_LRW_WMAX 32
+#endif
+constexpr int kWMax = SMC_LRW_WMAX;              // lanes one owner may take in a round
 constexpr int kWOvf = 1 << 16;                   // per-warp overflow LIFO (tasks)
 constexpr unsigned long long kWSegSlots = 32ull * kWSeg;
 constexpr unsigned long long kTasksPerWarp = kWSegSlots + kWOvf;
@@ -129,7 +133,7 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
       const int n_act = __popc(__ballot_sync(FULL, c > 0));
       if (n_act == 0 && ov == 0) break;
       // fair share: a heuristic (no result depends on the schedule, R-18)
-      const int W = n_act ? max(1, 32 / n_act) : 0;
+      const int W = n_act ? min(kWMax, max(1, 32 / n_act)) : 0;
       const int m = min(c, W);
       int incl = m;
 #pragma unroll
