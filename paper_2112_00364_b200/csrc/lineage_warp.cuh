@@ -37,6 +37,10 @@ constexpr int kWSeg = 256;                       // per-owner LIFO segment (task
 #define SMC_LRW_WMAX 32
 #endif
 constexpr int kWMax = SMC_LRW_WMAX;              // lanes one owner may take in a round
+#ifndef SMC_LRW_SMEM_SLOTS
+#define SMC_LRW_SMEM_SLOTS 0       // measured: 4, 8, 12 slots all slower (CRBD 59.3 -> 61.3-62.5 ms)
+#endif
+constexpr int kSm = SMC_LRW_SMEM_SLOTS;          // bottom slots of every owner segment kept in shared memory
 constexpr int kWOvf = 1 << 16;                   // per-warp overflow LIFO (tasks)
 constexpr unsigned long long kWSegSlots = 32ull * kWSeg;
 constexpr unsigned long long kTasksPerWarp = kWSegSlots + kWOvf;
@@ -44,6 +48,8 @@ constexpr unsigned long long kTasksPerWarp = kWSegSlots + kWOvf;
 template <class M>
 __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_kernel(LRArgs a, ModelConst C) {
   __shared__ typename M::Owner s_own[kWWarps][32];   // per-owner constants read by every lane
+  __shared__ double2 s_tsk[kWWarps][32 * (kSm > 0 ? kSm : 1)];                    // segment slots < kSm
+  __shared__ double s_tlam[kWWarps][M::kHasLam && kSm > 0 ? 32 * kSm : 1];
   __shared__ int s_start[kWWarps][32];               // round: lane where owner o's tasks start
   __shared__ int s_push[kWWarps][32];                // round: slots pushed for owner o
   __shared__ int s_det[kWWarps][32];                 // round: 1 detected, 3 rate guard
@@ -64,16 +70,44 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
   double2* T_sid = a.t.sid + tbase;
   double* T_lam = M::kHasLam ? a.t.lam + tbase : nullptr;
   unsigned short* T_own = a.t.owner + tbase;
+  // this warp's rows of the shared arrays (base addresses computed once)
+  typename M::Owner* w_own = s_own[warp];
+  int* w_start = s_start[warp];
+  int* w_push = s_push[warp];
+  int* w_det = s_det[warp];
+  int* w_ovn = s_ovn[warp];
+  int* w_ovtop = &s_ovtop[warp];
   if (threadIdx.x == 0) s_taskcap = 0;
   __syncthreads();
 
+  double2* w_tsk = s_tsk[warp];
+  double* w_tlam = s_tlam[warp];
+  // task records: the bottom kSm slots of each owner's segment live in shared
+  // memory (small stacks never leave the SM), the rest in this warp's region
   auto put = [&](unsigned long long slot, double s0, double lam0, unsigned long long id) {
-    T_sid[slot] = make_double2(s0, __longlong_as_double((long long)id));
+    const double2 v = make_double2(s0, __longlong_as_double((long long)id));
+    if (kSm > 0 && slot < kWSegSlots && (int)(slot % kWSeg) < kSm) {
+      const int k = (int)(slot / kWSeg) * kSm + (int)(slot % kWSeg);
+      w_tsk[k] = v;
+      if (M::kHasLam) w_tlam[k] = lam0;
+      return;
+    }
+    T_sid[slot] = v;
     if (M::kHasLam) T_lam[slot] = lam0;
+  };
+  auto get = [&](unsigned long long slot, double2& v, double& lam0) {
+    if (kSm > 0 && slot < kWSegSlots && (int)(slot % kWSeg) < kSm) {
+      const int k = (int)(slot / kWSeg) * kSm + (int)(slot % kWSeg);
+      v = w_tsk[k];
+      if (M::kHasLam) lam0 = w_tlam[k];
+      return;
+    }
+    v = T_sid[slot];
+    if (M::kHasLam) lam0 = T_lam[slot];
   };
   // overflow slot for owner o (-1: the warp's stack is full -> task-cap error)
   auto ovf_slot = [&](int o) -> long long {
-    const int q = atomicAdd(&s_ovtop[warp], 1);
+    const int q = atomicAdd(w_ovtop, 1);
     if (q >= kWOvf) { s_taskcap = 1; return -1; }
     const unsigned long long slot = kWSegSlots + (unsigned long long)q;
     T_own[slot] = (unsigned short)o;
@@ -89,7 +123,7 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
     unsigned batch = 0;
     if (lane == 0) {
       batch = atomicAdd(&p.ctrl->batch, 1u);
-      s_ovtop[warp] = 0;
+      *w_ovtop = 0;
     }
     batch = __shfl_sync(FULL, batch, 0);
     if (batch >= a.n_batches) break;
@@ -117,7 +151,7 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
           else slot = ovf_slot(lane);
           if (slot >= 0) put((unsigned long long)slot, s0, lam0, root_id(kk));
         };
-        if (!M::main_part(st, lw, r, C, s_own[warp][lane], K, push)) dead = 3;   // rate guard
+        if (!M::main_part(st, lw, r, C, w_own[lane], K, push)) dead = 3;   // rate guard
         roots += (unsigned long long)K;
         drw += 2ull * r.blk - (r.has_spare ? 1ull : 0ull);
         M::store(st, p.planes, p.n_local, i);
@@ -129,7 +163,7 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
     unsigned rounds = 0;
     for (;;) {
       if (dead) c = 0;                                  // a dead owner drops its stack
-      const int ov = min(*(volatile int*)&s_ovtop[warp], kWOvf);
+      const int ov = min(*(volatile int*)w_ovtop, kWOvf);
       const int n_act = __popc(__ballot_sync(FULL, c > 0));
       if (n_act == 0 && ov == 0) break;
       // fair share: a heuristic (no result depends on the schedule, R-18)
@@ -144,14 +178,14 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
       const int off = incl - m;
       const int T = min(__shfl_sync(FULL, incl, 31), 32);
       const int me = max(0, min(m, 32 - off));
-      s_start[warp][lane] = -1;
-      s_push[warp][lane] = 0;
-      s_det[warp][lane] = 0;
-      s_ovn[warp][lane] = 0;
+      w_start[lane] = -1;
+      w_push[lane] = 0;
+      w_det[lane] = 0;
+      w_ovn[lane] = 0;
       __syncwarp();
-      if (me > 0) s_start[warp][off] = lane;
+      if (me > 0) w_start[off] = lane;
       __syncwarp();
-      int o = s_start[warp][lane];
+      int o = w_start[lane];
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {               // owner of lane = last start at or below it
         const int t = __shfl_up_sync(FULL, o, d);
@@ -182,24 +216,21 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
       // new top up)
       double2 rec = make_double2(0.0, 0.0);
       double tl = 0.0;
-      if (run) {
-        rec = T_sid[slot];
-        if (M::kHasLam) tl = T_lam[slot];
-      }
-      if (lane == 0) s_ovtop[warp] = ov - min(ov, 32 - T);
+      if (run) get(slot, rec, tl);
+      if (lane == 0) *w_ovtop = ov - min(ov, 32 - T);
       __syncwarp();
       if (run) {
-        if (slot >= kWSegSlots) atomicAdd(&s_ovn[warp][ow], 1);
+        if (slot >= kWSegSlots) atomicAdd(&w_ovn[ow], 1);
         const uint32_t n_owner = (uint32_t)(p.shard_base + bbase + ow);
         drw += 2;
         NodeOut out;
-        const int res = M::node(rec.x, tl, (unsigned long long)__double_as_longlong(rec.y), s_own[warp][ow],
+        const int res = M::node(rec.x, tl, (unsigned long long)__double_as_longlong(rec.y), w_own[ow],
                                 n_owner, epoch, seed, rho, out);
         if (M::kHasLam && (res == NODE_BIRTH || res == NODE_GUARD)) drw += 2;   // daughters' noise block
         if (res == NODE_DETECTED || res == NODE_GUARD) {
-          atomicCAS(&s_det[warp][ow], 0, res == NODE_GUARD ? 3 : 1);
+          atomicCAS(&w_det[ow], 0, res == NODE_GUARD ? 3 : 1);
         } else if (res == NODE_BIRTH) {
-          const int b = base_ow + atomicAdd(&s_push[warp][ow], 2);
+          const int b = base_ow + atomicAdd(&w_push[ow], 2);
           const long long s1 = b < kWSeg ? (long long)ow * kWSeg + b : ovf_slot(ow);
           const long long s2 = b + 1 < kWSeg ? (long long)ow * kWSeg + b + 1 : ovf_slot(ow);
           if (s1 >= 0) put((unsigned long long)s1, out.s2, out.lb, out.idb);
@@ -209,12 +240,12 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
       __syncwarp();
       // owner updates
       if (dead == 0) {
-        nodes += (unsigned)(me + s_ovn[warp][lane]);
-        const int dc = s_det[warp][lane];
+        nodes += (unsigned)(me + w_ovn[lane]);
+        const int dc = w_det[lane];
         if (dc) dead = dc;
         else if (nodes > kSideNodeCap) dead = 2;
       }
-      c = min(c + s_push[warp][lane], kWSeg);
+      c = min(c + w_push[lane], kWSeg);
       ++rounds;
       __syncwarp();
     }
