@@ -1190,6 +1190,9 @@ __global__ void __launch_bounds__(kThreads) max_kernel(const double* lw, unsigne
 #ifndef SMC_FUSED_THREADS
 #define SMC_FUSED_THREADS 512
 #endif
+#ifndef SMC_FUSED_GALLOP
+#define SMC_FUSED_GALLOP 0
+#endif
 constexpr int kFT = SMC_FUSED_THREADS;   // threads per fused CTA
 #ifndef SMC_FUSED_MINB
 #define SMC_FUSED_MINB 2                 // resident CTAs per SM (register cap 64)
@@ -1416,13 +1419,36 @@ __global__ void __launch_bounds__(kFT, SMC_FUSED_MINB) resample_fused_kernel(Res
   if (!s_heavy) {
     // U chunks of 32 slots per iteration: U independent searches, then all
     // loads, then all stores (U*P 16-byte loads in flight per lane)
-    constexpr int U = P == 1 ? 4 : P == 2 ? 2 : 1;
+#ifndef SMC_FUSED_U2
+#define SMC_FUSED_U2 2
+#endif
+    constexpr int U = P == 1 ? 4 : P == 2 ? SMC_FUSED_U2 : 1;
+    const unsigned wspan = wB - wA;
     for (unsigned j0 = wA + lane; j0 < wB; j0 += 32 * U) {
       int src[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const unsigned j = j0 + 32 * u;
         int lo = wk0, hi = wk0 + wn - 1;                // first particle with O_k > j
+#if SMC_FUSED_GALLOP
+        // start at the proportional guess and gallop to a bracket (sources
+        // sit near their proportional position when weights are even)
+        if (j < wB) {
+          int g = wk0 + (int)(((unsigned long long)(j - wA) * (unsigned)wn) / max(1u, wspan));
+          g = min(max(g, wk0), wk0 + wn - 1);
+          if (s_O[g] > j) {
+            int st = 1;
+            hi = g;
+            while (g - st >= wk0 && s_O[g - st] > j) { hi = g - st; st <<= 1; }
+            lo = max(wk0, g - st);
+          } else {
+            int st = 1;
+            lo = g + 1;
+            while (g + st < wk0 + wn - 1 && s_O[g + st] <= j) { lo = g + st + 1; st <<= 1; }
+            hi = min(wk0 + wn - 1, g + st);
+          }
+        }
+#endif
         while (lo < hi) {
           const int mid = (lo + hi) >> 1;
           if (s_O[mid] > j) hi = mid; else lo = mid + 1;

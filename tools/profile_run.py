@@ -34,7 +34,9 @@ else:
     m = {"crbd": lambda: smc.Model.crbd(inputs.tree("tree90"), lineage=lin),
          "crbd_vr": lambda: smc.Model.crbd(inputs.tree("tree90"), analytic=True),
          "clads2": lambda: smc.Model.clads2(inputs.tree("tree90"), lineage=lin),
-         "seir": lambda: smc.Model.seir(inputs.seir_series())}[args.workload]()
+         "seir": lambda: smc.Model.seir(inputs.seir_series()),
+         "fig3": lambda: smc.Model.fig3(*inputs.FIG3_PARAMS),
+         "stackf": lambda: smc.Model.stackf(inputs.stackf_series(), inputs.STACKF_PARAMS[:3] + [1024.0])}[args.workload]()
     h = smc.Smc(m, args.n, 1)
     h.set_graph(False)     # ncu does not profile kernels inside conditional-graph bodies
     if args.workload == "crbd_vr":
