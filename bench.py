@@ -672,6 +672,8 @@ def sweep_line(args, name, wl, smc, torch, world, rank, pk, pk_kind, draw_peak, 
                                        frac=r["res_bytes"] / (r["res_ms"] * 1e-3) / 1e9 / hbm_peak,
                                        kernel=("resample_fused_kernel (one cooperative launch per epoch)"
                                                if r["fused"] else "reduce + anc_gather + finalize"),
+                                       traffic=((traffic(f"{wl['model']}:{N}:resample_fused_kernel") or {}).get("bytes")
+                                                if r["fused"] else None),
                                        note="per epoch at this N (latency-bound at 10^6; "
                                             "see workload 'resample' for the HBM-bound sizes)"),
                 roofline=dict(bound="alu", kernel=kname,

@@ -28,6 +28,22 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
   return c;
 }
 
+// Out-of-line Philox for call sites where code size matters more than the
+// call (the ClaDS2 kernel was instruction-fetch bound, ncu no_instruction
+// stalls): SMC_PHILOX_OOL=1 routes Rng::uniform and the side-tree blocks
+// through one copy of the rounds.  Same values either way.
+#ifndef SMC_PHILOX_OOL
+#define SMC_PHILOX_OOL 0
+#endif
+__device__ __noinline__ uint4 philox_call(uint4 c, uint32_t k0, uint32_t k1) { return philox4x32_10(c, k0, k1); }
+__device__ __forceinline__ uint4 philox_site(uint4 c, uint32_t k0, uint32_t k1) {
+#if SMC_PHILOX_OOL
+  return philox_call(c, k0, k1);
+#else
+  return philox4x32_10(c, k0, k1);
+#endif
+}
+
 // 53-bit integer of the hq conversion and the double u = z 2^-53 + 2^-54.
 __device__ __forceinline__ unsigned long long hq_bits(uint32_t x, uint32_t y) {
   return (unsigned long long)x ^ ((unsigned long long)y << 21);
@@ -47,7 +63,7 @@ struct Rng {
         spare(0.0), has_spare(false) {}
   __device__ __forceinline__ double uniform() {
     if (has_spare) { has_spare = false; return spare; }
-    const uint4 r = philox4x32_10(make_uint4(blk, t, n, 0u), k0, k1);
+    const uint4 r = philox_site(make_uint4(blk, t, n, 0u), k0, k1);
     ++blk;
     spare = hq(r.z, r.w);
     has_spare = true;

@@ -66,7 +66,7 @@ struct LRArgs {
 
 __device__ __forceinline__ uint4 side_block(unsigned long long seed, unsigned long long id,
                                             uint32_t n, uint32_t t, uint32_t tag) {
-  return philox4x32_10(make_uint4((uint32_t)id, (uint32_t)(id >> 32), n, (tag << 28) | t),
+  return philox_site(make_uint4((uint32_t)id, (uint32_t)(id >> 32), n, (tag << 28) | t),
                        (uint32_t)seed, (uint32_t)(seed >> 32));
 }
 __device__ __forceinline__ unsigned long long root_id(unsigned k) {
@@ -167,6 +167,29 @@ struct CrbdLR {
 // ---------------------------------------------------------------------------
 // ClaDS2 under §R-18 (with the §R-14b rate guard)
 // ---------------------------------------------------------------------------
+// ClaDS2 transcendental chains, optionally out of line (SMC_CLADS2_MATH_OOL=1,
+// value arguments only: nothing is forced to local memory); same formulas.
+#ifndef SMC_CLADS2_MATH_OOL
+#define SMC_CLADS2_MATH_OOL 0
+#endif
+#if SMC_CLADS2_MATH_OOL
+#define SMC_CLADS2_FN __device__ __noinline__
+#else
+#define SMC_CLADS2_FN __device__ __forceinline__
+#endif
+SMC_CLADS2_FN double clads2_bm(double u1, double u2) {            // N(0,1) (R-3, cos branch)
+  return 0.0 + 1.0 * (sqrt(-2.0 * log(u1)) * cospi(2.0 * u2));
+}
+SMC_CLADS2_FN double2 clads2_bm_pair(double u1, double u2) {      // Box-Muller pair (R-18)
+  const double rad = sqrt(-2.0 * log(u1));
+  double sn, cs;
+  sincospi(2.0 * u2, &sn, &cs);
+  return make_double2(rad * cs, rad * sn);
+}
+SMC_CLADS2_FN double clads2_rate(double alpha, double lam, double sigma, double z) {
+  return alpha * lam * exp(sigma * z);
+}
+
 struct Clads2LR {
 #ifndef SMC_LR_MINB_CLADS2
 #define SMC_LR_MINB_CLADS2 4
@@ -202,7 +225,7 @@ struct Clads2LR {
   __device__ static void push_pend(State& s, double v) { *pend_slot(s, s.sp) = v; s.sp = s.sp + 1; }
   __device__ static double pop_pend(State& s) { s.sp = s.sp - 1; return *pend_slot(s, s.sp); }
   __device__ static double daughter(const State& s, double lam, double z) {
-    return s.alpha * lam * exp(s.sigma * z);
+    return clads2_rate(s.alpha, lam, s.sigma, z);
   }
 
   template <class Push>
@@ -248,8 +271,8 @@ struct Clads2LR {
       r.consume(5, u);
       lw = lw + (-s.eps * s.lam * dt);
       t = t - dt;
-      const double zs = 0.0 + 1.0 * (sqrt(-2.0 * log(u[1])) * cospi(2.0 * u[2]));
-      const double zc = 0.0 + 1.0 * (sqrt(-2.0 * log(u[3])) * cospi(2.0 * u[4]));
+      const double zs = clads2_bm(u[1], u[2]);
+      const double zc = clads2_bm(u[3], u[4]);
       const double ls = daughter(s, s.lam, zs);
       if (Clads2::bad_rate(ls)) { killed = true; break; }
       push(t, ls, (unsigned)K);
@@ -259,8 +282,11 @@ struct Clads2LR {
     }
     if (!killed && internal) {
       lw = lw + log(s.lam);
-      const double zl = d_normal(r, 0.0, 1.0);
-      const double zr = d_normal(r, 0.0, 1.0);
+      double u[6];                           // z_l, z_r: the four uniforms of two d_normal calls
+      r.peek6(u);
+      r.consume(4, u);
+      const double zl = clads2_bm(u[0], u[1]);
+      const double zr = clads2_bm(u[2], u[3]);
       const double rl = daughter(s, s.lam, zl), rr = daughter(s, s.lam, zr);
       if (Clads2::bad_rate(rl) || Clads2::bad_rate(rr)) {
         killed = true;
@@ -291,12 +317,9 @@ struct Clads2LR {
 #if !SMC_CLADS2_SPEC_Z
     const uint4 Z = side_block(seed, id, n, t, kTagZ);
 #endif
-    const double rad = sqrt(-2.0 * log(hq(Z.x, Z.y)));
-    double sn, cs;
-    sincospi(2.0 * hq(Z.z, Z.w), &sn, &cs);      // Box-Muller pair at angle 2 pi u
-    const double za = rad * cs, zb = rad * sn;
-    out.la = ow.alpha * lam * exp(ow.sigma * za);
-    out.lb = ow.alpha * lam * exp(ow.sigma * zb);
+    const double2 zz = clads2_bm_pair(hq(Z.x, Z.y), hq(Z.z, Z.w));   // angle 2 pi u
+    out.la = clads2_rate(ow.alpha, lam, ow.sigma, zz.x);
+    out.lb = clads2_rate(ow.alpha, lam, ow.sigma, zz.y);
     if (Clads2::bad_rate(out.la) || Clads2::bad_rate(out.lb)) return NODE_GUARD;   // rate guard
     const uint4 Cb = side_block(seed, id, n, t, kTagChild);
     out.s2 = s - d;

@@ -45,6 +45,10 @@ constexpr int kWOvf = 1 << 16;                   // per-warp overflow LIFO (task
 constexpr unsigned long long kWSegSlots = 32ull * kWSeg;
 constexpr unsigned long long kTasksPerWarp = kWSegSlots + kWOvf;
 
+// fair share max(1, 32 / n) lanes per busy owner (table: no integer division in the round)
+__constant__ int c_wshare[33] = {0, 32, 16, 10, 8, 6, 5, 4, 4, 3, 3, 2, 2, 2, 2, 2, 2,
+                                 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
+
 template <class M>
 __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_kernel(LRArgs a, ModelConst C) {
   __shared__ typename M::Owner s_own[kWWarps][32];   // per-owner constants read by every lane
@@ -78,7 +82,14 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
   int* w_ovn = s_ovn[warp];
   int* w_ovtop = &s_ovtop[warp];
   if (threadIdx.x == 0) s_taskcap = 0;
+  // round scratch starts cleared; afterwards every owner clears its own entries
+  // when it reads them, and start markers carry the round number
+  w_start[lane] = -1;
+  w_push[lane] = 0;
+  w_det[lane] = 0;
+  w_ovn[lane] = 0;
   __syncthreads();
+  unsigned stamp = 0;                        // round number of this warp (start markers)
 
   double2* w_tsk = s_tsk[warp];
   double* w_tlam = s_tlam[warp];
@@ -167,7 +178,7 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
       const int n_act = __popc(__ballot_sync(FULL, c > 0));
       if (n_act == 0 && ov == 0) break;
       // fair share: a heuristic (no result depends on the schedule, R-18)
-      const int W = n_act ? min(kWMax, max(1, 32 / n_act)) : 0;
+      const int W = min(kWMax, c_wshare[n_act]);
       const int m = min(c, W);
       int incl = m;
 #pragma unroll
@@ -178,14 +189,11 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
       const int off = incl - m;
       const int T = min(__shfl_sync(FULL, incl, 31), 32);
       const int me = max(0, min(m, 32 - off));
-      w_start[lane] = -1;
-      w_push[lane] = 0;
-      w_det[lane] = 0;
-      w_ovn[lane] = 0;
+      ++stamp;
+      if (me > 0) w_start[off] = (int)((stamp << 5) | (unsigned)lane);
       __syncwarp();
-      if (me > 0) w_start[off] = lane;
-      __syncwarp();
-      int o = w_start[lane];
+      const int sv = w_start[lane];
+      int o = ((unsigned)sv >> 5) == stamp ? (sv & 31) : -1;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {               // owner of lane = last start at or below it
         const int t = __shfl_up_sync(FULL, o, d);
@@ -239,13 +247,16 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
       }
       __syncwarp();
       // owner updates
+      const int ovn = w_ovn[lane], dc = w_det[lane], pushed = w_push[lane];
+      w_ovn[lane] = 0;
+      w_det[lane] = 0;
+      w_push[lane] = 0;
       if (dead == 0) {
-        nodes += (unsigned)(me + w_ovn[lane]);
-        const int dc = w_det[lane];
+        nodes += (unsigned)(me + ovn);
         if (dc) dead = dc;
         else if (nodes > kSideNodeCap) dead = 2;
       }
-      c = min(c + w_push[lane], kWSeg);
+      c = min(c + pushed, kWSeg);
       ++rounds;
       __syncwarp();
     }

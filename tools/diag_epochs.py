@@ -7,7 +7,9 @@ import paper_2112_00364_b200 as smc
 wl = sys.argv[1] if len(sys.argv) > 1 else "crbd"
 m = {"crbd": lambda: smc.Model.crbd(inputs.tree("tree90"), lineage=True),
      "clads2": lambda: smc.Model.clads2(inputs.tree("tree90"), lineage=True),
-     "seir": lambda: smc.Model.seir(inputs.seir_series())}[wl]()
+     "seir": lambda: smc.Model.seir(inputs.seir_series()),
+     "fig3": lambda: smc.Model.fig3(*inputs.FIG3_PARAMS),
+     "stackf": lambda: smc.Model.stackf(inputs.stackf_series(), inputs.STACKF_PARAMS[:3] + [1024.0])}[wl]()
 h = smc.Smc(m, 1_000_000, 1)
 h.set_graph(False)
 h.set_timing(True)

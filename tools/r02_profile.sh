@@ -23,3 +23,12 @@ cap stackf_prop_e3 "propagate_kernel<smc::Stackf>" 3 stackf
 cap stackf_fused_e3 resample_fused_kernel 3 stackf
 cap c4_anc_gather_2p26 anc_gather_kernel 1 resample --n 67108864
 ls -la $O
+# export (the reports themselves are too large to bring back)
+for f in $O/*.ncu-rep; do
+  b=${f%.ncu-rep}
+  ncu -i $f --page raw --csv > ${b}_raw.csv 2>/dev/null
+  python tools/ncu_source.py $f 40 > ${b}_source.txt 2>/dev/null
+  python /root/repo/tools/ncu_phase_split.py $f > ${b}_phases.txt 2>/dev/null
+done
+du -sh $O/*.ncu-rep | sort -h | tail -3
+rm -f $O/*.ncu-rep
