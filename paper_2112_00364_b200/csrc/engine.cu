@@ -640,15 +640,15 @@ void launch_prop(smc_ctx* h, Shard& s, int cur) {
     // per 256 particles.  Occupancy query only, nothing enqueued (safe during
     // graph capture)
     int per_sm = 0, dev = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, propagate_kernel<M>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, propagate_kernel<M>, kPThreads, 0);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned long long need = (h->n_per + kThreads - 1) / kThreads;
+    const unsigned long long need = (h->n_per + kPThreads - 1) / kPThreads;
     h->prop_grid = M::kOneWave
         ? (int)std::min<unsigned long long>(need, (unsigned long long)std::max(1, per_sm * sms))
         : (int)need;
   }
-  propagate_kernel<M><<<(unsigned)h->prop_grid, kThreads, 0, h->stream>>>(a, h->mc);
+  propagate_kernel<M><<<(unsigned)h->prop_grid, kPThreads, 0, h->stream>>>(a, h->mc);
 }
 template <class M>
 void launch_prop_lr(smc_ctx* h, Shard& s, int cur) {

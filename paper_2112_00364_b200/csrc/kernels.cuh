@@ -24,6 +24,10 @@ namespace smc {
 typedef unsigned __int128 u128;
 
 constexpr int kThreads = 256;
+#ifndef SMC_PROP_THREADS
+#define SMC_PROP_THREADS 256
+#endif
+constexpr int kPThreads = SMC_PROP_THREADS;   // propagate_kernel CTA size (register cap kept: kMinBlocks x 256 threads)
 constexpr int kItems = 8;                  // particles per thread in a resampling tile (large N)
 constexpr int kItemsSmall = 2;             // ... below kSmallN particles per shard (more CTAs)
 constexpr unsigned long long kSmallN = 0;   // small tiles measured slower at 10^6 (per-CTA fixed costs dominate)
@@ -325,19 +329,19 @@ __device__ __forceinline__ void propagate_one(const PropArgs& a, const ModelCons
 // uneven models run one particle per thread and let the block scheduler
 // balance the load.
 template <class M>
-__global__ void __launch_bounds__(kThreads, M::kMinBlocks) propagate_kernel(PropArgs a, ModelConst C) {
-  __shared__ long long s_key[kThreads / 32];
-  __shared__ unsigned long long s_ovf[kThreads / 32];
-  __shared__ unsigned long long s_drw[kThreads / 32];
+__global__ void __launch_bounds__(kPThreads, M::kMinBlocks * (256 / kPThreads)) propagate_kernel(PropArgs a, ModelConst C) {
+  __shared__ long long s_key[kPThreads / 32];
+  __shared__ unsigned long long s_ovf[kPThreads / 32];
+  __shared__ unsigned long long s_drw[kPThreads / 32];
   if (*(volatile unsigned*)&a.ctrl->done) return;
   const unsigned epoch = a.ctrl->epoch;
   const bool carry = a.ctrl->carry != 0;               // R-19: no resample at the last checkpoint
   const unsigned long long seed = a.ctrl->seed;
   PropAcc acc;
   Diag dg;
-  const unsigned long long i0 = (unsigned long long)blockIdx.x * kThreads + threadIdx.x;
+  const unsigned long long i0 = (unsigned long long)blockIdx.x * kPThreads + threadIdx.x;
   if constexpr (M::kOneWave) {
-    for (unsigned long long i = i0; i < a.n_local; i += (unsigned long long)gridDim.x * kThreads)
+    for (unsigned long long i = i0; i < a.n_local; i += (unsigned long long)gridDim.x * kPThreads)
       propagate_one<M>(a, C, i, epoch, carry, seed, acc, dg);
   } else {
     if (i0 < a.n_local) propagate_one<M>(a, C, i0, epoch, carry, seed, acc, dg);
@@ -364,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, M::kMinBlocks) propagate_kernel(Prop
     end_alive += __shfl_xor_sync(0xffffffffu, end_alive, d);
     start_alive += __shfl_xor_sync(0xffffffffu, start_alive, d);
   }
-  __shared__ int s_cnt2[2][kThreads / 32];
+  __shared__ int s_cnt2[2][kPThreads / 32];
   if (lane == 0) { s_cnt2[0][warp] = end_alive; s_cnt2[1][warp] = start_alive; }
   __syncwarp();   // bar.red needs a converged warp (synccheck)
   const int any_bad = __syncthreads_or(bad);
@@ -372,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, M::kMinBlocks) propagate_kernel(Prop
     long long k = s_key[0];
     unsigned long long o = s_ovf[0], dr = s_drw[0];
     int n_end = s_cnt2[0][0], n_start = s_cnt2[1][0];
-    for (int w = 1; w < kThreads / 32; ++w) {
+    for (int w = 1; w < kPThreads / 32; ++w) {
       k = s_key[w] > k ? s_key[w] : k;
       o += s_ovf[w];
       dr += s_drw[w];
@@ -1395,6 +1399,9 @@ __global__ void __launch_bounds__(kFT, SMC_FUSED_MINB) resample_fused_kernel(Res
   }
   if (threadIdx.x == 0) s_O[blk] = (unsigned)gr.count_below(pre);   // O before the block
   __syncthreads();
+#ifdef SMC_DIAG_FUSED_NO_GATHER
+  return;   // diagnostics only (timing of phases 1-2a; results invalid)
+#endif
   // 2b: output slots.  Warp w's particles [w*32*ipt, (w+1)*32*ipt) (the
   // blocked items of its lanes) fill the contiguous slots [O_{first-1},
   // O_last); the lanes take consecutive slots and find their source by a
