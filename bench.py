@@ -692,16 +692,26 @@ def sweep_line(args, name, wl, smc, torch, world, rank, pk, pk_kind, draw_peak, 
         # output slot copies, with the stack-prefix copy and with the whole
         # user-defined stack (SMC_NO_STACK_PREFIX=1, same sweeps)
         per_slot = 16.0 * r["stack_planes"] / (r["resamples_per_sweep"] * steps * N)
-        os.environ["SMC_NO_STACK_PREFIX"] = "1"
-        try:
-            rf = bench_sweeps(sub_args, wl, smc, torch, world, rank)
-        finally:
-            os.environ.pop("SMC_NO_STACK_PREFIX", None)
-        rf["h"].close()
+        # like for like: both comparison runs materialise the gather in the
+        # resampling step (SMC_EAGER_GATHER=1), one copying the stack prefix,
+        # one the whole stack (SMC_NO_STACK_PREFIX=1)
+        runs = {}
+        for tag, env in (("prefix", {"SMC_EAGER_GATHER": "1"}),
+                         ("full", {"SMC_EAGER_GATHER": "1", "SMC_NO_STACK_PREFIX": "1"})):
+            os.environ.update(env)
+            try:
+                runs[tag] = bench_sweeps(sub_args, wl, smc, torch, world, rank)
+            finally:
+                for k in env:
+                    os.environ.pop(k, None)
+            runs[tag]["h"].close()
         line["stack_copy"] = dict(bytes_per_slot_prefix=per_slot, bytes_per_slot_full=float(r["state_bytes"]),
-                                  resample_ms_per_sweep_prefix=r["res_ms"] / steps,
-                                  resample_ms_per_sweep_full=rf["res_ms"] / steps,
-                                  ms_per_sweep_full=rf["t_ms"] / steps)
+                                  eager_resample_ms_per_sweep_prefix=runs["prefix"]["res_ms"] / steps,
+                                  eager_resample_ms_per_sweep_full=runs["full"]["res_ms"] / steps,
+                                  eager_ms_per_sweep_prefix=runs["prefix"]["t_ms"] / steps,
+                                  eager_ms_per_sweep_full=runs["full"]["t_ms"] / steps,
+                                  note="the headline run defers the gather into the next propagation "
+                                       "(DESIGN 7.7), which also copies only the stack prefix")
     if with_e2e:
         e = e2e_sweeps(sub_args, wl, smc, torch, r["h"], r["model"], min(steps, 3), world)
         tot = sum_over_ranks(torch, world, r["alive_steps"] / steps)

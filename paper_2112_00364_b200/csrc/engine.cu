@@ -99,6 +99,7 @@ struct smc_ctx {
   bool stack_prefix = true;       // §R-22 copy only the used stack prefix (env SMC_NO_STACK_PREFIX=1: off, diagnostics)
   int lr_grid = 0;                // persistent grid of the cooperative kernel
   bool lr_warp = true;            // warp-level cooperative kernel (env SMC_LR_KERNEL=cta: CTA rounds)
+  bool lazy = false;              // deferred gather (§7.7): one shard, out of place (env SMC_EAGER_GATHER=1: off)
   int prop_grid = 0;              // resident-CTA grid of propagate_kernel<M> (grid-stride)
   TaskArrays tasks{};
   int planes = 0;                 // 16-byte planes per particle
@@ -400,6 +401,7 @@ int reset_device(smc_ctx* h) {
   c.logz = 0.0;
   c.last_inc = 0.0;
   c.first_err = ~0ull;
+  c.gmap_id = 1;                        // first epoch: every particle reads its own slot
   c.seed = h->seed;
   c.ess_a = h->ess_a;
   c.ess_b = h->ess_b;
@@ -411,6 +413,8 @@ int reset_device(smc_ctx* h) {
     CU(cudaMemcpyAsync(s.ctrl, &c, sizeof(Ctrl), cudaMemcpyHostToDevice, h->stream));
     // pc = b0 = 0 and all fields zero; lw = 0; anc = identity
     CU(cudaMemsetAsync(s.planes[0], 0, (size_t)h->planes * h->n_per * 16, h->stream));
+    if (h->lazy)   // the first epoch reads the other buffer (deferred gather)
+      CU(cudaMemsetAsync(s.planes[1], 0, (size_t)h->planes * h->n_per * 16, h->stream));
     CU(cudaMemsetAsync(s.lw, 0, h->n_per * sizeof(double), h->stream));
   }
   for (auto& s : h->shards) {
@@ -575,6 +579,20 @@ int common_init(smc_ctx* h, const smc_model* m, unsigned long long n_per, int wo
     return fail(h, SMC_EINVAL, "SMC_FLAG_INPLACE needs a single shard (no cross-shard hole matching yet)");
   rc = plan_fused(h);
   if (rc) return rc;
+  {
+    // deferred gather: the resampling step writes ancestors only and the next
+    // propagation reads every state from its ancestor's slot (one shard,
+    // out-of-place runs of the models; the CTA cooperative kernel and the
+    // resampler-only handles keep the materialised gather)
+    // (measured: pays from 4 planes up — SEIR 85.6 -> 81.0 ms/sweep; CRBD's 2
+    // planes neutral, Fig. 3's single plane 10% slower — SMC_DEFERRED_GATHER=1
+    // forces it on for any model, SMC_EAGER_GATHER=1 off)
+    const char* eg = std::getenv("SMC_EAGER_GATHER");
+    const char* dg = std::getenv("SMC_DEFERRED_GATHER");
+    const bool want = (dg && dg[0] == '1') || h->planes >= 4;
+    h->lazy = want && world == 1 && n_local_shards == 1 && !h->inplace && h->kind != SMC_RESAMPLE_BENCH &&
+              (!h->lineage || h->lr_warp) && h->stack_prefix && !(eg && eg[0] == '1');
+  }
   h->shards.resize(n_local_shards);
   for (int i = 0; i < n_local_shards; ++i) {
     Shard& s = h->shards[i];
@@ -623,10 +641,16 @@ int barrier(smc_ctx* h) {
 }
 
 // ---- launches -----------------------------------------------------------------
+void set_prop_io(smc_ctx* h, Shard& s, int cur, PropArgs& a) {
+  a.planes = s.planes[cur];
+  a.lazy = h->lazy ? 1 : 0;
+  a.src_planes = h->lazy ? s.planes[cur ^ 1] : s.planes[cur];   // previous epoch's buffer
+  a.gmap = s.anc;
+}
 template <class M>
 void launch_prop(smc_ctx* h, Shard& s, int cur) {
   PropArgs a;
-  a.planes = s.planes[cur];
+  set_prop_io(h, s, cur, a);
   a.lw = s.lw;
   a.n_local = h->n_per;
   a.shard_base = s.base;
@@ -653,7 +677,7 @@ void launch_prop(smc_ctx* h, Shard& s, int cur) {
 template <class M>
 void launch_prop_lr(smc_ctx* h, Shard& s, int cur) {
   LRArgs a;
-  a.p.planes = s.planes[cur];
+  set_prop_io(h, s, cur, a.p);
   a.p.lw = s.lw;
   a.p.n_local = h->n_per;
   a.p.shard_base = s.base;
@@ -719,6 +743,7 @@ ResArgs res_args(smc_ctx* h, Shard& s, const double* lw, const uint4* src, int d
   a.tile_nz = s.scratch ? s.scratch + 3 * n : nullptr;
   a.tile_nz_excl = s.scratch ? s.scratch + 3 * n + h->n_tiles : nullptr;
   a.stk0 = a.stk_n = a.stk_per = a.sp_word = 0;
+  a.lazy = h->lazy ? 1 : 0;
   if (h->kind == SMC_CLADS2 && h->stack_prefix) {   // R-22: pending-rate stack, planes 2..4, sp = P5.z
     a.stk0 = 2; a.stk_n = 3; a.stk_per = 2; a.sp_word = 22;
   }
@@ -1346,14 +1371,37 @@ static int current_parity(smc_ctx* h) {
   return (int)(h->h_ctrl->epoch & 1);
 }
 
+// The buffer holding the current (post-resample) states of shard s.  Deferred
+// gather: after a resampling epoch they are the previous buffer seen through
+// the ancestors; materialise them into the buffer of parity `par` (the next
+// propagation's output, free until then).
+static int view_buffer(smc_ctx* h, Shard& s, int par, const uint4** out) {
+  *out = s.planes[par];
+  if (!h->lazy || !h->started || h->h_ctrl->done) return SMC_OK;
+  if (h->h_ctrl->gmap_id) {
+    *out = s.planes[par ^ 1];
+    return SMC_OK;
+  }
+  const unsigned g = (unsigned)std::min<unsigned long long>((h->n_per + 255) / 256, 4096ull);
+  gather_view_kernel<<<g, 256, 0, h->stream>>>(s.planes[par ^ 1], s.planes[par], s.anc, h->n_per, h->planes,
+                                                 s.base);
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(h->stream));
+  return SMC_OK;
+}
+
 int smc_state(smc_handle h, void* out, uint64_t bytes) {
   if (!h) return fail(h, SMC_EINVAL, "NULL handle");
   const uint64_t per = (uint64_t)h->planes * 16 * h->n_per;
   if (!out || bytes != per * h->shards.size()) return fail(h, SMC_EINVAL, "bad output size");
   const int par = current_parity(h);
   if (par < 0) return h->status;
-  for (size_t i = 0; i < h->shards.size(); ++i)
-    CU(cudaMemcpy((char*)out + i * per, h->shards[i].planes[par], per, cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < h->shards.size(); ++i) {
+    const uint4* src = nullptr;
+    int rc = view_buffer(h, h->shards[i], par, &src);
+    if (rc) return rc;
+    CU(cudaMemcpy((char*)out + i * per, src, per, cudaMemcpyDeviceToHost));
+  }
   return SMC_OK;
 }
 
@@ -1368,7 +1416,10 @@ int smc_fields(smc_handle h, double* out, uint64_t n_doubles) {
   const int par = current_parity(h);
   if (par < 0) return h->status;
   for (size_t si = 0; si < h->shards.size(); ++si) {
-    CU(cudaMemcpy(raw.data(), h->shards[si].planes[par], per, cudaMemcpyDeviceToHost));
+    const uint4* src = nullptr;
+    int rc = view_buffer(h, h->shards[si], par, &src);
+    if (rc) return rc;
+    CU(cudaMemcpy(raw.data(), src, per, cudaMemcpyDeviceToHost));
     for (uint64_t k = 0; k < h->n_per; ++k) {
       for (int p = 0; p < h->planes; ++p)
         for (int q = 0; q < 4; ++q) w[4 * p + q] = raw[4 * (p * h->n_per + k) + q];

@@ -73,6 +73,7 @@ struct Ctrl {
   unsigned bar_count, bar_gen;       // grid barrier of resample_fused_kernel
   unsigned long long guard_kills;    // ClaDS2 rate guard (R-14b): killed particle-steps
   unsigned long long stack_planes;   // stack models: 16-byte planes copied by the gathers (R-22/R-24)
+  unsigned gmap_id;                  // deferred gather: 1 = the next propagation reads its own slot
 };
 
 enum { ST_OK = 0, ST_REJECTED = 4, ST_NAN = 5, ST_OVERFLOW = 6 };
@@ -277,7 +278,13 @@ __device__ __forceinline__ unsigned long long quantize(double lw, double m) {
 // propagate
 // ============================================================================
 struct PropArgs {
-  uint4* planes;                 // current SoA planes of this shard
+  uint4* planes;                 // current SoA planes of this shard (the epoch's output)
+  // deferred gather (single shard): the epoch reads particle
+  // i's state from src_planes at its ancestor gmap[i] (at i when
+  // ctrl->gmap_id) and writes it to planes[i]; lazy = 0: in place (src = planes)
+  const uint4* src_planes;
+  const uint32_t* gmap;
+  int lazy;
   double* lw;                    // [n_local]
   unsigned long long n_local;    // also the plane stride
   unsigned long long shard_base; // global index of local particle 0
@@ -294,6 +301,25 @@ struct PropAcc {
   long long key = LLONG_MIN;
 };
 
+// Deferred gather: the source slot of output particle i (gmap holds global
+// ancestor indices; lazy runs have one shard, base 0), and the relocation of
+// state a model keeps in global memory while it runs (stack planes): copied
+// from the ancestor's slot below the stack pointer, then the model works on
+// its own slot.  Models that hold their whole state in registers: nothing.
+__device__ __forceinline__ unsigned long long gmap_src(const PropArgs& a, unsigned long long i) {
+  return (*(volatile unsigned*)&a.ctrl->gmap_id) ? i : (unsigned long long)__ldg(a.gmap + i);
+}
+template <class M> struct HasRelocate {
+  template <class T> static auto test(int) -> decltype(&T::relocate, char());
+  template <class T> static long test(...);
+  static constexpr bool value = sizeof(test<M>(0)) == sizeof(char);
+};
+template <class M>
+__device__ __forceinline__ void relocate(typename M::State& s, const uint4* src, uint4* dst,
+                                         unsigned long long st, unsigned long long si, unsigned long long di) {
+  if constexpr (HasRelocate<M>::value) M::relocate(s, src, dst, st, si, di);
+}
+
 // One particle: load, run blocks to the next checkpoint (or STOP), store.
 template <class M>
 __device__ __forceinline__ void propagate_one(const PropArgs& a, const ModelConst& C, unsigned long long i,
@@ -302,7 +328,13 @@ __device__ __forceinline__ void propagate_one(const PropArgs& a, const ModelCons
   double lw = carry ? a.lw[i] : 0.0;
   const unsigned long long ovf0 = dg.overflow;
   typename M::State s;
-  M::load(s, a.planes, a.n_local, i);
+  if (a.lazy) {                                   // the resampled state: ancestor's slot of the previous buffer
+    const unsigned long long si = gmap_src(a, i);
+    M::load(s, a.src_planes, a.n_local, si);
+    relocate<M>(s, a.src_planes, a.planes, a.n_local, si, i);
+  } else {
+    M::load(s, a.planes, a.n_local, i);
+  }
   if (M::pc(s) != kStop) {
     ++acc.start_alive;
     Rng r(seed, (uint32_t)(a.shard_base + i), epoch);
@@ -312,6 +344,8 @@ __device__ __forceinline__ void propagate_one(const PropArgs& a, const ModelCons
     }
     M::store(s, a.planes, a.n_local, i);
     acc.drw += 2ull * r.blk - (r.has_spare ? 1ull : 0ull);
+  } else if (a.lazy) {
+    M::store(s, a.planes, a.n_local, i);          // finished particles move too
   }
   acc.end_alive += M::pc(s) != kStop;
   a.lw[i] = lw;
@@ -394,6 +428,18 @@ __global__ void __launch_bounds__(kPThreads, M::kMinBlocks * (256 / kPThreads)) 
   if (dg.guard) atomicAdd(&a.ctrl->guard_kills, dg.guard);   // rare (ClaDS2 only)
 }
 
+// Deferred gather, state dumps only (smc_state / smc_fields): materialise the
+// resampled states dst[i] = src[anc[i]] (every plane) into the buffer the next
+// propagation will overwrite anyway.
+__global__ void gather_view_kernel(const uint4* src, uint4* dst, const uint32_t* anc,
+                                   unsigned long long n, int planes, unsigned long long base) {
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long a = (unsigned long long)anc[i] - base;
+    for (int p = 0; p < planes; ++p) dst[(unsigned long long)p * n + i] = src[(unsigned long long)p * n + a];
+  }
+}
+
 // anc[i] = base + i (identity before the first resample)
 __global__ void iota_kernel(uint32_t* anc, unsigned long long n, unsigned long long base) {
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -433,6 +479,7 @@ struct ResArgs {
   // stk_per entries per plane whose pointer is word sp_word of the particle's
   // planes; only the first ceil(sp / stk_per) stack planes are copied
   int stk0, stk_n, stk_per, sp_word;
+  int lazy;                           // deferred gather: ancestors only, no state copies (§7.7)
 };
 
 // First stack plane of particle `src` that need not be copied (planes
@@ -693,7 +740,7 @@ __global__ void __launch_bounds__(kThreads, 4) anc_gather_kernel(ResArgs a) {
     // buffer so the epoch's buffer parity holds), ancestors unchanged
     uint4* dst = a.dst_planes[a.rank];
     const int np = P > 0 ? P : a.planes;
-    for (int k = threadIdx.x; k < cnt; k += kThreads) {
+    for (int k = threadIdx.x; k < (a.lazy ? 0 : cnt); k += kThreads) {   // deferred gather: none
       const int lo = stack_skip_lo(a, a.src_planes, base + k);
       for (int p = 0; p < np; p = next_plane(a, p, lo))
         if (copy_plane(a, p, lo))
@@ -784,6 +831,10 @@ __global__ void __launch_bounds__(kThreads, 4) anc_gather_kernel(ResArgs a) {
     uint4* dst = a.dst_planes[dshard];
     const int skip = stack_skip_lo(a, a.src_planes, src);     // R-22: stack prefix only
     if (a.stk_n) stk_copied += planes_copied(a, skip);
+    if (a.lazy) {                                             // deferred gather: ancestors only
+      a.dst_anc[dshard][dl] = (uint32_t)(a.shard_base + src);
+      continue;
+    }
     if (P > 0) {
       uint4 v[P > 0 ? P : 1];
 #pragma unroll
@@ -1067,15 +1118,18 @@ __device__ __noinline__ void finalize_body(const FinArgs& a) {
     } else if (G.alive == 0) {
       c->logz = c->logz + inc;                         // final: no resample (R-6)
       c->done = 1;
+      c->gmap_id = 1;
     } else if (ess_resample(W, total_q2(a.recB + par * a.world, a.world), a.n_total, c->ess_a,
                             c->ess_b)) {
       c->logz = c->logz + inc;
       c->resamples = c->resamples + 1;
       c->carry = 0;
       c->epoch = epoch + 1;
+      c->gmap_id = 0;                                  // next epoch reads through the ancestors
     } else {
       c->carry = 1;                                    // weights accumulate (R-19)
       c->epoch = epoch + 1;
+      c->gmap_id = 1;                                  // states stay where they are
     }
   }
   c->batch = 0;
@@ -1376,8 +1430,9 @@ __global__ void __launch_bounds__(kFT, SMC_FUSED_MINB) resample_fused_kernel(Res
   if (G.alive == 0) return;                             // final epoch: no resample
   uint4* dst = a.dst_planes[a.rank];
   if (!ess_resample(tot, q2t, a.n_total, c->ess_a, c->ess_b)) {
-    for (int k = threadIdx.x; k < cnt; k += kFT)        // ESS high: identity copy (R-19)
-      copy_particle<P>(a, dst, base + k, base + k, stack_skip_lo(a, a.src_planes, base + k));
+    if (!a.lazy)                                        // (deferred gather: states stay put)
+      for (int k = threadIdx.x; k < cnt; k += kFT)      // ESS high: identity copy (R-19)
+        copy_particle<P>(a, dst, base + k, base + k, stack_skip_lo(a, a.src_planes, base + k));
     return;
   }
   const unsigned long long seed = c->seed;
@@ -1430,7 +1485,9 @@ __global__ void __launch_bounds__(kFT, SMC_FUSED_MINB) resample_fused_kernel(Res
 #define SMC_FUSED_U2 2
 #endif
     constexpr int U = P == 1 ? 4 : P == 2 ? SMC_FUSED_U2 : 1;
+#if SMC_FUSED_GALLOP
     const unsigned wspan = wB - wA;
+#endif
     for (unsigned j0 = wA + lane; j0 < wB; j0 += 32 * U) {
       int src[U];
 #pragma unroll
@@ -1464,18 +1521,22 @@ __global__ void __launch_bounds__(kFT, SMC_FUSED_MINB) resample_fused_kernel(Res
       }
       if (P > 0 && P <= 2 && a.stk_n == 0) {            // whole-particle copies
         uint4 v[U][P > 0 && P <= 2 ? P : 1];
+        if (!a.lazy) {
 #pragma unroll
-        for (int u = 0; u < U; ++u)
+          for (int u = 0; u < U; ++u)
 #pragma unroll
-          for (int p = 0; p < (P > 0 && P <= 2 ? P : 1); ++p)
-            if (j0 + 32 * u < wB)
-              v[u][p] = __ldg(a.src_planes + (unsigned long long)p * a.n_local + base + src[u]);
+            for (int p = 0; p < (P > 0 && P <= 2 ? P : 1); ++p)
+              if (j0 + 32 * u < wB)
+                v[u][p] = __ldg(a.src_planes + (unsigned long long)p * a.n_local + base + src[u]);
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const unsigned j = j0 + 32 * u;
           if (j < wB) {
+            if (!a.lazy) {
 #pragma unroll
-            for (int p = 0; p < (P > 0 && P <= 2 ? P : 1); ++p) dst[(unsigned long long)p * a.n_local + j] = v[u][p];
+              for (int p = 0; p < (P > 0 && P <= 2 ? P : 1); ++p) dst[(unsigned long long)p * a.n_local + j] = v[u][p];
+            }
             anc[j] = (uint32_t)(a.shard_base + base + src[u]);
           }
         }
@@ -1487,7 +1548,7 @@ __global__ void __launch_bounds__(kFT, SMC_FUSED_MINB) resample_fused_kernel(Res
             const unsigned long long sp = base + src[u];
             const int skip = stack_skip_lo(a, a.src_planes, sp);
             if (a.stk_n) stk_copied += planes_copied(a, skip);
-            copy_particle<P>(a, dst, sp, j, skip);
+            if (!a.lazy) copy_particle<P>(a, dst, sp, j, skip);
             anc[j] = (uint32_t)(a.shard_base + sp);
           }
         }
@@ -1504,7 +1565,7 @@ __global__ void __launch_bounds__(kFT, SMC_FUSED_MINB) resample_fused_kernel(Res
       const unsigned long long src = base + lo;
       const int skip = stack_skip_lo(a, a.src_planes, src);
       if (a.stk_n) stk_copied += planes_copied(a, skip);
-      copy_particle<P>(a, dst, src, j, skip);
+      if (!a.lazy) copy_particle<P>(a, dst, src, j, skip);
       anc[j] = (uint32_t)(a.shard_base + src);
     }
   }

@@ -219,6 +219,14 @@ struct Clads2LR {
     stp(P, st, 5, i, make_uint4((uint32_t)s.pc, (uint32_t)s.branch, (uint32_t)s.sp, 0u));
   }
   __device__ static int pc(const State& s) { return s.pc; }
+  // deferred gather: the ancestor's pending-rate planes below sp move to this slot
+  __device__ static void relocate(State& s, const uint4* src, uint4* dst, unsigned long long st,
+                                  unsigned long long si, unsigned long long di) {
+    for (int k = 0; 2 * k < s.sp; ++k)
+      dst[(unsigned long long)(2 + k) * st + di] = __ldg(src + (unsigned long long)(2 + k) * st + si);
+    s.P = dst;
+    s.i = di;
+  }
   __device__ static double* pend_slot(const State& s, int k) {
     return reinterpret_cast<double*>(s.P + (unsigned long long)(2 + (k >> 1)) * s.st + s.i) + (k & 1);
   }

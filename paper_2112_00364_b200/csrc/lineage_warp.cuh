@@ -151,7 +151,13 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
     __syncwarp();
     if (valid) {
       typename M::State st;
-      M::load(st, p.planes, p.n_local, i);
+      if (p.lazy) {                              // deferred gather: from the ancestor's slot
+        const unsigned long long si = gmap_src(p, i);
+        M::load(st, p.src_planes, p.n_local, si);
+        relocate<M>(st, p.src_planes, p.planes, p.n_local, si, i);
+      } else {
+        M::load(st, p.planes, p.n_local, i);
+      }
       if (M::pc(st) != kStop) {
         act = true;
         ++n_start;
@@ -166,6 +172,8 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
         roots += (unsigned long long)K;
         drw += 2ull * r.blk - (r.has_spare ? 1ull : 0ull);
         M::store(st, p.planes, p.n_local, i);
+      } else if (p.lazy) {
+        M::store(st, p.planes, p.n_local, i);    // finished particles move too
       }
       alive_end = M::pc(st) != kStop;
     }

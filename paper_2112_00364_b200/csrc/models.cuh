@@ -498,6 +498,14 @@ struct Stackf {
     stp(P, st, 0, i, make_uint4((uint32_t)s.pc, (uint32_t)s.sp, (uint32_t)rb, (uint32_t)(rb >> 32)));
   }
   __device__ static int pc(const State& s) { return s.pc; }
+  // deferred gather: the ancestor's stack planes below sp move to this slot
+  __device__ static void relocate(State& s, const uint4* src, uint4* dst, unsigned long long st,
+                                  unsigned long long si, unsigned long long di) {
+    for (int q = 0; 16 * q < s.sp; ++q)
+      dst[(unsigned long long)(1 + q) * st + di] = __ldg(src + (unsigned long long)(1 + q) * st + si);
+    s.P = dst;
+    s.i = di;
+  }
   // the stack plane holding byte offset `off`
   __device__ static uint4* plane(const State& s, int off) {
     return s.P + (unsigned long long)(1 + off / 16) * s.st + s.i;

@@ -493,3 +493,26 @@ def test_resampler_bench_size_vs_oracle(smc):
         want = a64[:, None] * words + (4 * p + torch.arange(4, device=dev, dtype=torch.int64))[None, :]
         assert torch.equal(got[p].to(torch.int64), want)
     assert r.distinct() == len(np.unique(ref["anc"]))
+
+
+# ------------------------------------------------------------- deferred gather
+@pytest.mark.parametrize("kind,data,params,N", [
+    (oracle.CRBD_LR, "tree90", inputs.CRBD_PARAMS, 20_000),
+    (oracle.CRBD, "tree5", inputs.CRBD_PARAMS, 4099),
+    (oracle.FIG3, None, inputs.FIG3_PARAMS, 30_001),
+    (oracle.SSM, "ssm", inputs.SSM_PARAMS, 5000),
+    (oracle.SEIR, "seir", None, 3000),
+    (oracle.CLADS2_LR, "tree90", inputs.CLADS2_PARAMS, 10_000),
+    (oracle.STACKF, "stackf", inputs.STACKF_PARAMS, 5000),
+])
+@pytest.mark.parametrize("mode", ["deferred", "eager"])
+def test_gather_modes_vs_oracle(smc, monkeypatch, kind, data, params, N, mode):
+    """The deferred gather (resampling writes ancestors only, the next epoch
+    reads each state from its ancestor's slot) and the
+    materialised one, forced on models whose default is the other mode,
+    per epoch against the oracle."""
+    monkeypatch.setenv("SMC_DEFERRED_GATHER" if mode == "deferred" else "SMC_EAGER_GATHER", "1")
+    data = {"tree5": lambda: inputs.tree("tree5"), "tree90": lambda: inputs.tree("tree90"),
+            "ssm": lambda: inputs.ssm_series(50), "seir": inputs.seir_series,
+            "stackf": inputs.stackf_series}.get(data, lambda: data)()
+    run_pair(smc, kind, data, params, N, 21)
