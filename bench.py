@@ -330,7 +330,12 @@ def bench_sweeps(args, wl, smc, torch, world, rank):
         n_loc = st["n_local"]
         # algorithmic resample bytes of the sweep: per resample N*20 + S*(D + N),
         # plus the final epoch's reduce (8 B/particle)
-        if st["stack_planes"]:
+        if st["deferred_gather"]:
+            # the resampling step writes ancestors only (DESIGN 7.7): two lw
+            # passes + the anc write; the state copy happens inside the next
+            # propagation and is not counted here
+            res_bytes += st["resamples"] * n_loc * 20 + 8 * n_loc
+        elif st["stack_planes"]:
             # stack models: the gathers copy only the planes below the stack pointer
             res_bytes += st["resamples"] * n_loc * 20 + 16 * st["stack_planes"] * 2 + 8 * n_loc
         else:
@@ -349,6 +354,7 @@ def bench_sweeps(args, wl, smc, torch, world, rank):
                 res_bytes=res_bytes, resamples_per_sweep=n_resamples / args.steps,
                 res_ms=res_ms, draws=draws, guard=guard, alive_steps=alive_steps, epochs=steps_done,
                 stack_planes=stack_planes, state_bytes=st["state_bytes"],
+                deferred=bool(st["deferred_gather"]),
                 launches=launches, fused=fused, clocks=clk.summary(torch.cuda.current_device()),
                 logz=float(np.mean(logzs)))
 
@@ -674,6 +680,10 @@ def sweep_line(args, name, wl, smc, torch, world, rank, pk, pk_kind, draw_peak, 
                                                if r["fused"] else "reduce + anc_gather + finalize"),
                                        traffic=((traffic(f"{wl['model']}:{N}:resample_fused_kernel") or {}).get("bytes")
                                                 if r["fused"] else None),
+                                       state_gather=("deferred into the next propagation (DESIGN 7.7): "
+                                                     "B_alg = N*20 per resample, no state bytes"
+                                                     if r["deferred"] else
+                                                     "in the resampling step: B_alg = N*(20+S) + S*D"),
                                        note="per epoch at this N (latency-bound at 10^6; "
                                             "see workload 'resample' for the HBM-bound sizes)"),
                 roofline=dict(bound="alu", kernel=kname,

@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define SMC_ABI_VERSION 1
+#define SMC_ABI_VERSION 2
 
 typedef enum {
   SMC_OK = 0,
@@ -161,6 +161,10 @@ typedef struct {
                                        (R-14b; under SMC_FLAG_LINEAGE_RNG a step
                                        whose side trees both detect and break the guard may
                                        be counted either way)                               */
+  uint32_t deferred_gather;         /* 1: resampling writes ancestors only and the next
+                                       propagation reads each state from its ancestor's slot
+                                       (DESIGN.md 7.7); 0: the resampling step copies states  */
+  uint32_t reserved0;
 } smc_stats_t;
 
 /* --- lifetime --------------------------------------------------------------- */

@@ -60,7 +60,9 @@ class smc_stats_t(C.Structure):
                 ("timed_epochs", C.c_uint64), ("side_roots", C.c_uint64),
                 ("max_rounds", C.c_uint32), ("max_side_nodes", C.c_uint32),
                 ("distinct", C.c_uint64), ("ms_kernel", C.c_double * 4),
-                ("stack_planes", C.c_uint64), ("guard_kills", C.c_uint64)]
+                ("stack_planes", C.c_uint64), ("guard_kills", C.c_uint64),
+                ("deferred_gather", C.c_uint32),
+                ("reserved0", C.c_uint32)]
 
 
 ALLGATHER_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)

@@ -1440,6 +1440,7 @@ int smc_stats(smc_handle h, smc_stats_t* out) {
   out->state_bytes = (uint32_t)h->planes * 16;
   out->first_error_particle = -1;
   out->status = h->status;
+  out->deferred_gather = h->lazy ? 1u : 0u;
   out->ms_propagate = h->ms_propagate;
   out->ms_resample = h->ms_resample;
   out->timed_epochs = h->timed_epochs;

@@ -34,7 +34,7 @@ def test_library_exports_every_declared_symbol():
                          text=True).stdout
     exported = set(re.findall(r" T (smc_[a-z0-9_]+)$", out, flags=re.M))
     assert set(syms) <= exported
-    assert lib.smc_abi_version() == 1
+    assert lib.smc_abi_version() == 2
 
 
 def test_binding_covers_header():
