@@ -89,7 +89,10 @@ struct OwnerClads2 { double eps, alpha, sigma, pb; };
 // ---------------------------------------------------------------------------
 struct CrbdLR {
   static constexpr int kLRMinBlocks = SMC_LR_MINB;   // 64 registers at 128 threads
-  static constexpr int kLRWMinBlocks = 8;            // warp-level kernel (lineage_warp.cuh)
+#ifndef SMC_LRW_MINB_CRBD
+#define SMC_LRW_MINB_CRBD 6      // 80 registers, 24 B spills (8: 64 regs, 84 B spills; 7: 72 regs): measured 55.8 / 55.7 / 54.4 ms at 8 / 7 / 6
+#endif
+  static constexpr int kLRWMinBlocks = SMC_LRW_MINB_CRBD;   // warp-level kernel (lineage_warp.cuh)
   typedef Crbd::State State;
   typedef OwnerCrbd Owner;
   static constexpr int kPlanes = Crbd::kPlanes;

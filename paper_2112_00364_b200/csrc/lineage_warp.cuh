@@ -37,6 +37,9 @@ constexpr int kWSeg = 256;                       // per-owner LIFO segment (task
 #define SMC_LRW_WMAX 32
 #endif
 constexpr int kWMax = SMC_LRW_WMAX;              // lanes one owner may take in a round
+#ifndef SMC_LRW_FASTMAP
+#define SMC_LRW_FASTMAP 1
+#endif
 #ifndef SMC_LRW_SMEM_SLOTS
 #define SMC_LRW_SMEM_SLOTS 0       // measured: 4, 8, 12 slots all slower (CRBD 59.3 -> 61.3-62.5 ms)
 #endif
@@ -70,6 +73,7 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
   const bool carry = p.ctrl->carry != 0;
   const double rho = C.p[0];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned le_mask = 0xffffffffu >> (31 - lane);   // lanes 0..lane
   const unsigned long long tbase = ((unsigned long long)blockIdx.x * kWWarps + warp) * kTasksPerWarp;
   double2* T_sid = a.t.sid + tbase;
   double* T_lam = M::kHasLam ? a.t.lam + tbase : nullptr;
@@ -126,7 +130,7 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
   };
 
   long long key = LLONG_MIN;
-  unsigned long long n_end = 0, n_start = 0, drw = 0, ovf = 0, roots = 0, guard = 0;
+  unsigned n_end = 0, n_start = 0, drw = 0, ovf = 0, roots = 0, guard = 0;   // per lane (32-bit: fewer registers)
   bool bad = false;
   unsigned max_rounds = 0, max_nodes = 0;
 
@@ -169,8 +173,8 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
           if (slot >= 0) put((unsigned long long)slot, s0, lam0, root_id(kk));
         };
         if (!M::main_part(st, lw, r, C, w_own[lane], K, push)) dead = 3;   // rate guard
-        roots += (unsigned long long)K;
-        drw += 2ull * r.blk - (r.has_spare ? 1ull : 0ull);
+        roots += (unsigned)K;
+        drw += 2u * r.blk - (r.has_spare ? 1u : 0u);
         M::store(st, p.planes, p.n_local, i);
       } else if (p.lazy) {
         M::store(st, p.planes, p.n_local, i);    // finished particles move too
@@ -188,6 +192,43 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
       // fair share: a heuristic (no result depends on the schedule, R-18)
       const int W = min(kWMax, c_wshare[n_act]);
       const int m = min(c, W);
+#if SMC_LRW_FASTMAP
+      // lane offsets: inclusive scan of m (0..32) from six bit-sliced ballots
+      // (independent, no shuffle chain); the owner of a lane is the last task
+      // range starting at or below it: a bitmask of range starts (one
+      // redux.sync) and one shared-memory read of (owner, its count) at that start
+      int incl = 0, T = 0;
+#pragma unroll
+      for (int b = 0; b < 6; ++b) {
+        const unsigned bb = __ballot_sync(FULL, (m >> b) & 1);
+        incl += __popc(bb & le_mask) << b;
+        T += __popc(bb) << b;
+      }
+      T = min(T, 32);
+      const int off = incl - m;
+      const int me = max(0, min(m, 32 - off));
+      if (me > 0) w_start[off] = (c << 5) | lane;
+      const unsigned starts = __reduce_or_sync(FULL, me > 0 ? (1u << off) : 0u);
+      __syncwarp();
+      bool have = false;
+      unsigned long long slot = 0;
+      int ow = 0;
+      if (lane < T) {
+        const int s0 = 31 - __clz(starts & le_mask);   // this lane's range start
+        const int sv = w_start[s0];
+        have = true;
+        ow = sv & 31;
+        slot = (unsigned long long)ow * kWSeg + (unsigned long long)((sv >> 5) - 1 - (lane - s0));
+      } else if (lane - T < ov) {
+        have = true;
+        slot = kWSegSlots + (unsigned long long)(ov - 1 - (lane - T));
+        ow = (int)T_own[slot];
+      }
+      c -= me;                                          // pops (the owner's base for pushes)
+      const int bd = __shfl_sync(FULL, c | (dead << 16), ow);
+      const int base_ow = bd & 0xffff;
+      const int dead_ow = bd >> 16;
+#else
       int incl = m;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
@@ -226,6 +267,7 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
       c -= me;                                          // pops (the owner's base for pushes)
       const int base_ow = __shfl_sync(FULL, c, ow);
       const int dead_ow = __shfl_sync(FULL, dead, ow);
+#endif
       const bool run = have && dead_ow == 0;
       // read the popped records before any lane pushes: pushes reuse the
       // popped slots (segment: from the owner's base up; overflow: from the
@@ -297,23 +339,23 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
   for (int d = 16; d > 0; d >>= 1) {
     const long long t = __shfl_xor_sync(FULL, key, d);
     key = t > key ? t : key;
-    n_end += __shfl_xor_sync(FULL, n_end, d);
-    n_start += __shfl_xor_sync(FULL, n_start, d);
-    drw += __shfl_xor_sync(FULL, drw, d);
-    ovf += __shfl_xor_sync(FULL, ovf, d);
-    roots += __shfl_xor_sync(FULL, roots, d);
-    guard += __shfl_xor_sync(FULL, guard, d);
-    max_nodes = max(max_nodes, __shfl_xor_sync(FULL, max_nodes, d));
   }
+  n_end = __reduce_add_sync(FULL, n_end);
+  n_start = __reduce_add_sync(FULL, n_start);
+  drw = __reduce_add_sync(FULL, drw);
+  ovf = __reduce_add_sync(FULL, ovf);
+  roots = __reduce_add_sync(FULL, roots);
+  guard = __reduce_add_sync(FULL, guard);
+  max_nodes = __reduce_max_sync(FULL, max_nodes);
   bad = __any_sync(FULL, bad);
   if (lane == 0) {
     s_key[warp] = key;
     s_acc[0][warp] = n_end;
     s_acc[1][warp] = n_start;
     s_acc[2][warp] = drw;
-    if (ovf) atomicAdd(&p.ctrl->overflow, ovf);
-    if (guard) atomicAdd(&p.ctrl->guard_kills, guard);
-    if (roots) atomicAdd(&p.ctrl->side_roots, roots);
+    if (ovf) atomicAdd(&p.ctrl->overflow, (unsigned long long)ovf);
+    if (guard) atomicAdd(&p.ctrl->guard_kills, (unsigned long long)guard);
+    if (roots) atomicAdd(&p.ctrl->side_roots, (unsigned long long)roots);
     atomicMax(&p.ctrl->max_side_nodes, max_nodes);
     atomicMax(&p.ctrl->max_rounds, max_rounds);
   }
