@@ -597,6 +597,17 @@ def run_ours(args, wl):
                                             "mean_log_z", "phase_ms", "draws_per_particle_step",
                                             "roofline", "resample_roofline", "clocks", "config",
                                             "guard_kills_per_particle_step", "gpu_launches") if k in sl}
+        # configs[1] under the per-particle sequential stream (R-11: one thread
+        # walks its whole side tree; the headline uses the lineage-keyed R-18)
+        seq_args = argparse.Namespace(**vars(args))
+        seq_args.rng, seq_args.workload = "sequential", "crbd (sequential stream)"
+        sl = sweep_line(seq_args, "crbd", wl, smc, torch, world, rank, pk, pk_kind, draw_peak,
+                        with_e2e=False, with_cpu=False)
+        subs["c1_crbd_sequential_rng"] = {k: sl[k] for k in ("metric", "value", "unit", "ms_per_step",
+                                                             "sweeps_per_s", "mean_log_z", "phase_ms",
+                                                             "draws_per_particle_step", "roofline",
+                                                             "resample_roofline", "clocks", "config",
+                                                             "gpu_launches") if k in sl}
         for lg in (26, 28):
             rl = resample_line(args, smc, torch, world, rank, pk, pk_kind, n=1 << lg, sigma=1.0)
             subs[f"c4_resample_2p{lg}"] = {k: rl[k] for k in ("metric", "value", "unit", "ms_per_step",

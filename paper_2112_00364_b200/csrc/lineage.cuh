@@ -82,7 +82,7 @@ enum { NODE_LEAF = 0, NODE_DETECTED = 1, NODE_BIRTH = 2, NODE_GUARD = 3 };
 
 // Per-owner constants kept in shared memory during phase 2.
 struct OwnerCrbd { double inv_tot, pb; };
-struct OwnerClads2 { double eps, alpha, sigma, pb; };
+struct OwnerClads2 { double opeps, alpha, sigma, pb; };   // opeps = 1 + eps
 
 // ---------------------------------------------------------------------------
 // CRBD under §R-18
@@ -90,7 +90,7 @@ struct OwnerClads2 { double eps, alpha, sigma, pb; };
 struct CrbdLR {
   static constexpr int kLRMinBlocks = SMC_LR_MINB;   // 64 registers at 128 threads
 #ifndef SMC_LRW_MINB_CRBD
-#define SMC_LRW_MINB_CRBD 6      // 80 registers, 24 B spills (8: 64 regs, 84 B spills; 7: 72 regs): measured 55.8 / 55.7 / 54.4 ms at 8 / 7 / 6
+#define SMC_LRW_MINB_CRBD 5      // 5 CTAs/SM (up to 102 regs): measured 55.8 / 55.7 / 54.7 / 53.6 / 56.4 ms at 8 / 7 / 6 / 5 / 4
 #endif
   static constexpr int kLRWMinBlocks = SMC_LRW_MINB_CRBD;   // warp-level kernel (lineage_warp.cuh)
   typedef Crbd::State State;
@@ -259,7 +259,7 @@ struct Clads2LR {
       s.branch = 0;
       s.pc = 1;
     }
-    ow.eps = s.eps; ow.alpha = s.alpha; ow.sigma = s.sigma;
+    ow.opeps = 1.0 + s.eps; ow.alpha = s.alpha; ow.sigma = s.sigma;
     ow.pb = 1.0 / (1.0 + s.eps);
     const double* b = C.table + 4 * s.branch;
     const double tp = __ldg(b), tc = __ldg(b + 1);
@@ -322,8 +322,12 @@ struct Clads2LR {
     const uint4 Z = side_block(seed, id, n, t, kTagZ);     // speculative: independent of B
 #endif
     const double u0 = hq(B.x, B.y), u1 = hq(B.z, B.w);
-    const double d = -log(u0) / (lam * (1.0 + ow.eps));
-    if (d > s) return u1 < rho ? NODE_DETECTED : NODE_LEAF;
+    // d = -log(u0) / (lam (1 + eps)) ~ Exp(lam (1 + eps)); the test d > s is
+    // taken as -log(u0) > s lam (1 + eps) (no division; the same decision up
+    // to rounding, like the CUDA/glibc ulp differences), d itself only for a birth
+    const double rate = lam * ow.opeps;
+    const double nl = -log(u0);
+    if (nl > s * rate) return u1 < rho ? NODE_DETECTED : NODE_LEAF;
     if (!(u1 < ow.pb)) return NODE_LEAF;
 #if !SMC_CLADS2_SPEC_Z
     const uint4 Z = side_block(seed, id, n, t, kTagZ);
@@ -333,7 +337,7 @@ struct Clads2LR {
     out.lb = clads2_rate(ow.alpha, lam, ow.sigma, zz.y);
     if (Clads2::bad_rate(out.la) || Clads2::bad_rate(out.lb)) return NODE_GUARD;   // rate guard
     const uint4 Cb = side_block(seed, id, n, t, kTagChild);
-    out.s2 = s - d;
+    out.s2 = s - nl / rate;
     out.ida = ((unsigned long long)Cb.y << 32) | Cb.x;
     out.idb = ((unsigned long long)Cb.w << 32) | Cb.z;
     return NODE_BIRTH;

@@ -40,6 +40,9 @@ constexpr int kWMax = SMC_LRW_WMAX;              // lanes one owner may take in 
 #ifndef SMC_LRW_FASTMAP
 #define SMC_LRW_FASTMAP 1
 #endif
+#ifndef SMC_LRW_BALLOTPUSH
+#define SMC_LRW_BALLOTPUSH 0      // ballot-ranked pushes instead of shared atomics: measured slower (CRBD 53.8 -> 57.0, ClaDS2 188 -> 196 ms)
+#endif
 #ifndef SMC_LRW_SMEM_SLOTS
 #define SMC_LRW_SMEM_SLOTS 0       // measured: 4, 8, 12 slots all slower (CRBD 59.3 -> 61.3-62.5 ms)
 #endif
@@ -93,7 +96,9 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
   w_det[lane] = 0;
   w_ovn[lane] = 0;
   __syncthreads();
+#if !SMC_LRW_FASTMAP
   unsigned stamp = 0;                        // round number of this warp (start markers)
+#endif
 
   double2* w_tsk = s_tsk[warp];
   double* w_tlam = s_tlam[warp];
@@ -212,9 +217,9 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
       __syncwarp();
       bool have = false;
       unsigned long long slot = 0;
-      int ow = 0;
+      int ow = 0, s0 = 0;
       if (lane < T) {
-        const int s0 = 31 - __clz(starts & le_mask);   // this lane's range start
+        s0 = 31 - __clz(starts & le_mask);             // this lane's range start
         const int sv = w_start[s0];
         have = true;
         ow = sv & 31;
@@ -277,6 +282,60 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
       if (run) get(slot, rec, tl);
       if (lane == 0) *w_ovtop = ov - min(ov, 32 - T);
       __syncwarp();
+#if SMC_LRW_FASTMAP && SMC_LRW_BALLOTPUSH
+      // segment lanes (lane < T: contiguous per owner) report births and
+      // detections by ballot: a birth's rank among its owner's births gives its
+      // push slots, the owner reads its counts from its own lane range — no
+      // shared-memory atomics; tasks from the overflow stack keep the atomic
+      // path and push to the overflow stack
+      int res = -1;
+      NodeOut out;
+      if (run) {
+        const uint32_t n_owner = (uint32_t)(p.shard_base + bbase + ow);
+        drw += 2;
+        res = M::node(rec.x, tl, (unsigned long long)__double_as_longlong(rec.y), w_own[ow],
+                      n_owner, epoch, seed, rho, out);
+        if (M::kHasLam && (res == NODE_BIRTH || res == NODE_GUARD)) drw += 2;   // daughters' noise block
+      }
+      const bool segl = lane < T;
+      const unsigned bmask = __ballot_sync(FULL, segl && res == NODE_BIRTH);
+      const unsigned dmask = __ballot_sync(FULL, segl && res == NODE_DETECTED);
+      const unsigned gmask = __ballot_sync(FULL, segl && res == NODE_GUARD);
+      if (segl && res == NODE_BIRTH) {
+        const int b = base_ow + 2 * __popc(bmask & (le_mask >> 1) & (0xffffffffu << s0));
+        const long long s1 = b < kWSeg ? (long long)ow * kWSeg + b : ovf_slot(ow);
+        const long long s2 = b + 1 < kWSeg ? (long long)ow * kWSeg + b + 1 : ovf_slot(ow);
+        if (s1 >= 0) put((unsigned long long)s1, out.s2, out.lb, out.idb);
+        if (s2 >= 0) put((unsigned long long)s2, out.s2, out.la, out.ida);   // first daughter on top
+      } else if (run && !segl) {                        // a task from the overflow stack
+        atomicAdd(&w_ovn[ow], 1);
+        if (res == NODE_DETECTED || res == NODE_GUARD) {
+          atomicCAS(&w_det[ow], 0, res == NODE_GUARD ? 3 : 1);
+        } else if (res == NODE_BIRTH) {
+          const long long s1 = ovf_slot(ow), s2 = ovf_slot(ow);
+          if (s1 >= 0) put((unsigned long long)s1, out.s2, out.lb, out.idb);
+          if (s2 >= 0) put((unsigned long long)s2, out.s2, out.la, out.ida);
+        }
+      }
+      __syncwarp();
+      // owner updates: its lane range [off, off + me) of this round
+      const unsigned rmask = me > 0 ? ((me >= 32 ? 0xffffffffu : ((1u << me) - 1u)) << off) : 0u;
+      int dc = (dmask & rmask) ? 1 : ((gmask & rmask) ? 3 : 0);
+      const int pushed = 2 * __popc(bmask & rmask);
+      int ovn = 0;
+      if (ov) {                                         // (warp-uniform) overflow tasks this round
+        ovn = w_ovn[lane];
+        const int dco = w_det[lane];
+        w_ovn[lane] = 0;
+        w_det[lane] = 0;
+        if (!dc) dc = dco;
+      }
+      if (dead == 0) {
+        nodes += (unsigned)(me + ovn);
+        if (dc) dead = dc;
+        else if (nodes > kSideNodeCap) dead = 2;
+      }
+#else
       if (run) {
         if (slot >= kWSegSlots) atomicAdd(&w_ovn[ow], 1);
         const uint32_t n_owner = (uint32_t)(p.shard_base + bbase + ow);
@@ -306,6 +365,7 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
         if (dc) dead = dc;
         else if (nodes > kSideNodeCap) dead = 2;
       }
+#endif
       c = min(c + pushed, kWSeg);
       ++rounds;
       __syncwarp();
