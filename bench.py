@@ -647,16 +647,38 @@ def sweep_line(args, name, wl, smc, torch, world, rank, pk, pk_kind, draw_peak, 
     cpu = None
     if rank == 0 and with_cpu and world == 1:
         cpu = oracle_sweep_rate(wl, budget_s=args.cpu_budget)
+    spec = None
     if lin:
-        # speculative side-tree nodes inflate the GPU's count: the algorithmic
-        # count is the oracle's, on a sample of the same workload (the
-        # cpu_baseline sweep when it ran, else a 20000-particle sweep)
+        # Under R-18 the GPU's count depends on its visiting order (speculative
+        # side-tree nodes evaluated before a detection elsewhere stops the tree,
+        # and nodes a depth-first walk would have reached first but that were
+        # pruned).  The algorithmic count is the oracle's for the SAME particle
+        # system: per-sweep counts vary ~2x between seeds, so a different seed
+        # is no reference.  The oracle sweep of the sample (the cpu_baseline
+        # sweep when it ran, else 20000 particles; seed 12345) is repeated on
+        # the GPU with the same N and seed — identical particles, ancestors and
+        # weights (parity) — and the ratio oracle/GPU of the two counts scales
+        # the GPU's count at the bench size.
         try:
             if cpu:
-                odps = cpu[3]["draws"] / max(cpu[3]["alive_particle_steps"], 1)
-                osample = cpu[1]
+                ost, osample = cpu[3], cpu[1]
             else:
-                odps, osample = oracle_draws_per_step(wl, n=20000)
+                _, osample, _, ost = oracle_sweep_rate(wl, n_cap=20000, budget_s=0.0)
+            odraws = ost["draws"]
+            n_s = int(osample.split("N=")[1].split()[0])
+            hs = smc.Smc(model_for(smc, wl, rng, False), n_s, seed=12345)
+            ea, eb = (int(x) for x in ess.split("/"))
+            hs.set_ess_threshold(ea, eb)
+            hs.run()
+            gst = hs.stats()
+            hs.close()
+            ratio = odraws / max(gst["draws"], 1)
+            if gst["alive_particle_steps"] != ost["alive_particle_steps"]:
+                raise RuntimeError("sample sweeps differ (GPU vs oracle particle-steps)")
+            odps = gdps * ratio
+            spec = dict(sample=osample, oracle_draws=odraws, gpu_draws=gst["draws"],
+                        oracle_over_gpu=ratio,
+                        oracle_draws_per_particle_step_sample=odraws / max(ost["alive_particle_steps"], 1))
         except Exception as e:  # noqa: BLE001  (the oracle is a reported baseline, not the product)
             odps, osample = None, f"oracle unavailable: {e}"
     else:
@@ -682,7 +704,10 @@ def sweep_line(args, name, wl, smc, torch, world, rank, pk, pk_kind, draw_peak, 
                 phase_ms=dict(propagate=r["prop_ms"] / steps, resample=r["res_ms"] / steps,
                               propagate_share=prop_frac),
                 draws_per_particle_step=dict(oracle=odps, oracle_sample=osample, gpu=gdps,
-                                             note="gpu counts speculative side-tree nodes (R-18)"
+                                             seed_matched=spec,
+                                             note=("algorithmic = the GPU count of this run x the oracle/GPU "
+                                                   "ratio of a seed-matched sample sweep (the GPU's visiting "
+                                                   "order changes which side-tree nodes it draws, R-18)")
                                              if lin else "identical streams"),
                 resample_roofline=dict(bound="hbm", achieved=r["res_bytes"] / (r["res_ms"] * 1e-3) / 1e9,
                                        peak=hbm_peak, unit="GB/s",

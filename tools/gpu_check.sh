@@ -1,6 +1,6 @@
-# Round-2 re-entry check: GPU tests, default bench line, smoke.
-O=gpurun_out/r02x; mkdir -p $O
+# Full GPU check: tests, smoke, default bench line (configs[1] + sub-results)
+O=gpurun_out/${1:-r02c}; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/smi.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -x -q > $O/pytest.log 2>&1; echo pytest=$?; tail -3 $O/pytest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke=$?; tail -1 $O/smoke.log
-timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo bench=$?; tail -c 3000 $O/bench.json
+timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo bench=$?; tail -c 600 $O/bench.json; tail -3 $O/bench.err
