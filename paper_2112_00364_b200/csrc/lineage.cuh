@@ -39,6 +39,9 @@ namespace smc {
 #ifndef SMC_LR_OPT
 #define SMC_LR_OPT 1
 #endif
+#ifndef SMC_CLADS2_MERGED
+#define SMC_CLADS2_MERGED 1     // ClaDS2 branch walk: one loop body for hidden events and the node split
+#endif
 #ifndef SMC_CLADS2_SPEC_Z
 #define SMC_CLADS2_SPEC_Z 1     // ClaDS2 nodes: daughters' noise block before the event test (measured -1.3%)
 #endif
@@ -265,6 +268,60 @@ struct Clads2LR {
     const double tp = __ldg(b), tc = __ldg(b + 1);
     const bool internal = __ldg(b + 2) != 0.0;
     const bool first_left = __ldg(b + 3) != 0.0;
+#if SMC_CLADS2_MERGED
+    // One loop body for the hidden events of the branch and the split at its
+    // end (internal child): both turn four uniforms into two normals and two
+    // daughter rates of the current rate, so the Box-Muller and exp code is
+    // emitted once (half the instruction footprint of this phase, and lanes
+    // at a split run it together with lanes at an event).  Same draws, same
+    // formulas and the same order of checks as the two-loop form below.
+    bool killed = Clads2::bad_rate(s.lam);
+    double t = tp;
+    bool split = false;
+    while (!killed) {
+      double u[6];
+      r.peek6(u);
+      if (!split) {
+        const double dt = -log(u[0]) / s.lam;
+        if (t - dt <= tc) {
+          r.consume(1, u);
+          lw = lw + (-s.eps * s.lam * (t - tc));
+          if (!internal) break;
+          lw = lw + log(s.lam);
+          split = true;
+          continue;
+        }
+        r.consume(5, u);
+        lw = lw + (-s.eps * s.lam * dt);
+        t = t - dt;
+      } else {
+        r.consume(4, u);                     // z_l, z_r: the four uniforms of two d_normal calls
+      }
+      const double a1 = split ? u[0] : u[1], a2 = split ? u[1] : u[2];   // (selects: no local array)
+      const double b1 = split ? u[2] : u[3], b2 = split ? u[3] : u[4];
+      const double z1 = clads2_bm(a1, a2);
+      const double z2 = clads2_bm(b1, b2);
+      const double r1 = daughter(s, s.lam, z1), r2 = daughter(s, s.lam, z2);
+      if (split) {
+        if (Clads2::bad_rate(r1) || Clads2::bad_rate(r2)) {
+          killed = true;
+        } else {
+          push_pend(s, first_left ? r2 : r1);
+          s.lam = first_left ? r1 : r2;
+        }
+        break;
+      }
+      if (Clads2::bad_rate(r1)) { killed = true; break; }   // the side lineage (z_side)
+      push(t, r1, (unsigned)K);
+      ++K;
+      s.lam = r2;                                           // the continuing lineage (z_cont)
+      if (Clads2::bad_rate(s.lam)) { killed = true; break; }
+    }
+    if (!killed && !internal) {
+      lw = lw + log(rho);
+      if (s.branch + 1 < C.n) s.lam = pop_pend(s);
+    }
+#else
     bool killed = Clads2::bad_rate(s.lam);
     double t = tp;
     while (!killed) {
@@ -309,6 +366,7 @@ struct Clads2LR {
       lw = lw + log(rho);
       if (s.branch + 1 < C.n) s.lam = pop_pend(s);
     }
+#endif
     if (killed) lw = -INFINITY;
     s.branch = s.branch + 1;
     s.pc = (s.branch == C.n) ? kStop : 1;

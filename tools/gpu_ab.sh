@@ -1,9 +1,6 @@
-# A/B of resampling launch shapes and the deferred gather for CRBD (diagnostic)
-O=gpurun_out/r02z4; mkdir -p $O
-timeout 900 bash tools/variants.sh crbd "" "-DSMC_FUSED_MINB=1" "-DSMC_FUSED_THREADS=1024 -DSMC_FUSED_MINB=1" "-DSMC_FUSED_THREADS=256 -DSMC_FUSED_MINB=4" "" 2>&1 | tee $O/variants_crbd.txt
-for v in 0 1; do
-  SMC_DEFERRED_GATHER=$v timeout 300 python bench.py --workload crbd --only --no-e2e --no-cpu-baseline --steps 3 --warmup 3 2>/dev/null | python -c "
-import json,sys
-d=json.loads(sys.stdin.read().strip().split('\n')[-1])
-print('crbd deferred=$v ms/sweep %.2f prop %.2f res %.2f' % (d['ms_per_step'], d['phase_ms']['propagate'], d['phase_ms']['resample']))" | tee -a $O/deferred.txt
-done
+# A/B: ClaDS2 merged branch-walk body, Philox unrolling (diagnostic)
+O=gpurun_out/r02z5; mkdir -p $O
+timeout 1200 python -m pytest tests -m gpu -x -q -k "clads2 or CLADS2" > $O/pytest_lr.log 2>&1; echo pytest=$?; tail -2 $O/pytest_lr.log
+timeout 1500 bash tools/variants.sh clads2 "" "-DSMC_CLADS2_MERGED=0" "-DSMC_PHILOX_UNROLL=5" "" 2>&1 | tee $O/variants_clads2.txt
+timeout 600 bash tools/variants.sh crbd "" "-DSMC_PHILOX_UNROLL=5" 2>&1 | tee $O/variants_crbd.txt
+timeout 600 bash tools/variants.sh seir "" "-DSMC_PHILOX_UNROLL=5" 2>&1 | tee $O/variants_seir.txt
