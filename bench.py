@@ -32,15 +32,15 @@ sys.path.insert(0, ROOT)
 import inputs  # noqa: E402
 
 WORKLOADS = {
-    "crbd": dict(config=1, model="crbd", tree="tree90", n=1_000_000,
+    "crbd": dict(config=1, model="crbd", tree="tree90", n=1_000_000, oracle_n=60000,
                  desc="CRBD birth-death, synthetic 90-tip Yule tree (tree90), priors Gamma(1,1)/Gamma(1,0.5)"),
     "crbd_vr": dict(config=None, model="crbd", tree="tree90", n=1_000_000, analytic=True, ess="1/2",
                     desc="CRBD on tree90 with the Sec. 5.3 variance reduction: 2E(t) per hidden event "
                          "instead of a simulated side tree (DESIGN R-20) and ESS-triggered resampling "
                          "at ESS < N/2 (R-19)"),
-    "clads2": dict(config=2, model="clads2", tree="tree90", n=1_000_000,
+    "clads2": dict(config=2, model="clads2", tree="tree90", n=1_000_000, oracle_n=40000,
                    desc="ClaDS2 lineage-specific-rate birth-death on tree90"),
-    "seir": dict(config=3, model="seir", n=1_000_000,
+    "seir": dict(config=3, model="seir", n=1_000_000, oracle_n=30000,
                  desc="vector-borne-disease SEIR on the synthetic 182-day case series seir182"),
     "geometric": dict(config=None, model="geometric", n=1_000_000,
                       desc="weighted geometric, Fig. 2 (p=0.5, w=1.5): particles reach b_stop at "
@@ -188,7 +188,12 @@ def oracle_sweep_rate(wl, budget_s=15.0, n_cap=None):
         data, params = inputs.seir_series(), None
     n = 1000
     ea, eb = (int(x) for x in getattr(oracle_sweep_rate, "ess", "1/1").split("/"))
-    if budget_s > 0:
+    if budget_s > 0 and wl.get("oracle_n"):
+        # a fixed sample per workload (~5-10 s on one core), so the cpu_baseline
+        # leg and the reference arm time the same computation: per-particle-step
+        # cost depends on the particle system, which depends on N and the seed
+        n = wl["oracle_n"]
+    elif budget_s > 0:
         t0 = time.perf_counter()
         s = oracle.Smc(kind, data, params, n, 12345)
         s.set_ess(ea, eb)
@@ -249,7 +254,7 @@ def run_reference(args, wl):
     else:
         vals = []
         for _ in range(args.warmup):
-            oracle_sweep_rate(wl, budget_s=3.0)
+            oracle_sweep_rate(wl, budget_s=0.0, n_cap=1000)
         for _ in range(args.steps):
             pss, sample, dt, st = oracle_sweep_rate(wl, budget_s=8.0)
             vals.append(pss)

@@ -19,10 +19,10 @@ constexpr double kHalfLog2Pi = 0.9189385332046727417803297364056176;
 
 // U = rounds per loop iteration: 10 = straight-line code; a partly rolled loop
 // trades two loop instructions per iteration for code size.  Measured (B200,
-// ms per sweep): the per-particle sequential stream (Rng::uniform, used by the
-// one-thread-per-particle models) rolled to 5: SEIR 82.6 -> 80.2 (its sampler
-// code is instruction-fetch bound); every Philox rolled to 5: CRBD 53.6 -> 58.4,
-// ClaDS2 181.4 -> 197.6 (their inner loops fit the instruction cache).
+// ms per sweep): the sequential stream rolled to 5: SEIR 82.7 -> 80.4 (its
+// sampler code is instruction-fetch bound), sequential-stream CRBD 198 -> 213;
+// every Philox rolled to 5: CRBD 53.6 -> 58.4, ClaDS2 181.4 -> 197.6.  So only
+// the binomial samplers use the rolled form (Rng::uniform_compact).
 #ifndef SMC_PHILOX_UNROLL_SEQ
 #define SMC_PHILOX_UNROLL_SEQ 5
 #endif
@@ -74,11 +74,17 @@ struct Rng {
         spare(0.0), has_spare(false) {}
   __device__ __forceinline__ double uniform() {
     if (has_spare) { has_spare = false; return spare; }
-#if SMC_PHILOX_OOL
     const uint4 r = philox_site(make_uint4(blk, t, n, 0u), k0, k1);
-#else
+    ++blk;
+    spare = hq(r.z, r.w);
+    has_spare = true;
+    return hq(r.x, r.y);
+  }
+  // The same stream from a partly rolled Philox (smaller code; for the
+  // out-of-line binomial samplers, whose kernel is instruction-fetch bound).
+  __device__ __forceinline__ double uniform_compact() {
+    if (has_spare) { has_spare = false; return spare; }
     const uint4 r = philox4x32_10<SMC_PHILOX_UNROLL_SEQ>(make_uint4(blk, t, n, 0u), k0, k1);
-#endif
     ++blk;
     spare = hq(r.z, r.w);
     has_spare = true;
@@ -189,7 +195,7 @@ __device__ __noinline__ long long d_binomial_inv(Rng& r, long long n, double p) 
   const double sr = p / q;
   const double a = (double)(n + 1) * sr;
   double pr = exp((double)n * log1p(-p));
-  double u = r.uniform();
+  double u = r.uniform_compact();
   long long x = 0;
   while (x < n && u > pr) {
     u = u - pr;
@@ -210,8 +216,8 @@ __device__ __noinline__ long long d_binomial_btrs(Rng& r, long long n, double p,
   bool have_h = false;
   double h = 0.0, alpha = 0.0, lpq = 0.0;
   for (;;) {
-    const double U = r.uniform() - 0.5;
-    const double V = r.uniform();
+    const double U = r.uniform_compact() - 0.5;
+    const double V = r.uniform_compact();
     const double us = 0.5 - fabs(U);
     const double kd = floor((2.0 * a / us + b) * U + c);
     if (kd < 0.0 || kd > nd) continue;

@@ -42,6 +42,9 @@ namespace smc {
 #ifndef SMC_CLADS2_MERGED
 #define SMC_CLADS2_MERGED 1     // ClaDS2 branch walk: one loop body for hidden events and the node split
 #endif
+#ifndef SMC_CLADS2_LAZYPEEK
+#define SMC_CLADS2_LAZYPEEK 0   // Philox blocks only as far as used: measured slower (181.0 -> 187.0 ms; the look-ahead ILP wins)
+#endif
 #ifndef SMC_CLADS2_SPEC_Z
 #define SMC_CLADS2_SPEC_Z 1     // ClaDS2 nodes: daughters' noise block before the event test (measured -1.3%)
 #endif
@@ -280,6 +283,50 @@ struct Clads2LR {
     bool split = false;
     while (!killed) {
       double u[6];
+#if SMC_CLADS2_LAZYPEEK
+      // the Philox blocks of the next uniforms only as far as they are used:
+      // block A always (u0, the event time); B for the normals of an event or
+      // a split; C only for an event that starts on a fresh block (5 uniforms)
+      const uint4 A = philox4x32_10(make_uint4(r.blk, r.t, r.n, 0u), r.k0, r.k1);
+      {
+        const double a0 = hq(A.x, A.y), a1 = hq(A.z, A.w);
+        u[0] = r.has_spare ? r.spare : a0;
+        u[1] = r.has_spare ? a0 : a1;
+        u[2] = a1;
+      }
+      double dt = 0.0;
+      if (!split) {
+        dt = -log(u[0]) / s.lam;
+        if (t - dt <= tc) {
+          r.consume(1, u);
+          lw = lw + (-s.eps * s.lam * (t - tc));
+          if (!internal) break;
+          lw = lw + log(s.lam);
+          split = true;
+          continue;
+        }
+      }
+      {
+        const uint4 B = philox4x32_10(make_uint4(r.blk + 1u, r.t, r.n, 0u), r.k0, r.k1);
+        const double b0 = hq(B.x, B.y), b1 = hq(B.z, B.w);
+        if (r.has_spare) {
+          u[3] = b0; u[4] = b1; u[5] = 0.0;
+        } else {
+          u[2] = b0; u[3] = b1; u[4] = 0.0; u[5] = 0.0;
+          if (!split) {
+            const uint4 Cc = philox4x32_10(make_uint4(r.blk + 2u, r.t, r.n, 0u), r.k0, r.k1);
+            u[4] = hq(Cc.x, Cc.y); u[5] = hq(Cc.z, Cc.w);
+          }
+        }
+      }
+      if (!split) {
+        r.consume(5, u);
+        lw = lw + (-s.eps * s.lam * dt);
+        t = t - dt;
+      } else {
+        r.consume(4, u);                     // z_l, z_r: the four uniforms of two d_normal calls
+      }
+#else
       r.peek6(u);
       if (!split) {
         const double dt = -log(u[0]) / s.lam;
@@ -297,6 +344,7 @@ struct Clads2LR {
       } else {
         r.consume(4, u);                     // z_l, z_r: the four uniforms of two d_normal calls
       }
+#endif
       const double a1 = split ? u[0] : u[1], a2 = split ? u[1] : u[2];   // (selects: no local array)
       const double b1 = split ? u[2] : u[3], b2 = split ? u[3] : u[4];
       const double z1 = clads2_bm(a1, a2);

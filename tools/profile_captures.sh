@@ -1,14 +1,17 @@
-# Round-2 evidence: per-epoch phase times, a cold launch list of one CRBD sweep
+# Evidence for a round: per-epoch phase times, cold launch lists of one sweep
 # (step mode, so ncu sees every kernel), and one `ncu --set full` capture per
 # dominant kernel.  Diagnostic only (numbers under a profiler are not bench values).
+#   bash tools/profile_captures.sh [out-dir]   (default gpurun_out/r02f)
 export PATH=/usr/local/cuda/bin:$PATH
-O=gpurun_out/r02p
+O=${1:-gpurun_out/r02f}
 mkdir -p $O
 for wl in crbd clads2 seir; do python tools/diag_epochs.py $wl > $O/epochs_$wl.txt 2>&1; done
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_crbd_sweep.csv \
     python tools/profile_run.py --workload crbd > /dev/null 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_clads2_sweep.csv \
     python tools/profile_run.py --workload clads2 > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_seir_sweep.csv \
+    python tools/profile_run.py --workload seir > /dev/null 2>&1
 cap() {   # name kernel-regex skip workload [extra args]
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:$2 --launch-skip $3 --launch-count 1 \
       -o $O/$1 -f python tools/profile_run.py --workload $4 ${@:5} > $O/$1.log 2>&1
