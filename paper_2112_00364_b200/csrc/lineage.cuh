@@ -39,6 +39,9 @@ namespace smc {
 #ifndef SMC_LR_OPT
 #define SMC_LR_OPT 1
 #endif
+#ifndef SMC_CRBD_RECIP
+#define SMC_CRBD_RECIP 1        // CRBD branch walk: -log(u) * (1/lambda) instead of a division
+#endif
 #ifndef SMC_CLADS2_MERGED
 #define SMC_CLADS2_MERGED 1     // ClaDS2 branch walk: one loop body for hidden events and the node split
 #endif
@@ -135,12 +138,22 @@ struct CrbdLR {
     double t = tp;
     K = 0;
     // hidden event times t -= Exp(lambda) until t <= t_c (the draws of d_exp,
-    // two per iteration from one Philox block, their logs side by side)
+    // two per iteration from one Philox block, their logs side by side; the
+    // division by lambda as a multiplication by 1/lambda: ulp-level
+    // differences, like the CUDA/glibc log differences)
+#if SMC_CRBD_RECIP
+    const double il = 1.0 / s.lambda;
+#endif
     for (;;) {
       double u[3];
       r.peek2(u);
-      const double t1 = t - (-log(u[0]) / s.lambda);
-      const double e1 = -log(u[1]) / s.lambda;
+#if SMC_CRBD_RECIP
+      const double t1 = t - (-log_u(u[0]) * il);
+      const double e1 = -log_u(u[1]) * il;
+#else
+      const double t1 = t - (-log_u(u[0]) / s.lambda);
+      const double e1 = -log_u(u[1]) / s.lambda;
+#endif
       if (t1 <= tc) { r.consume(1, u); break; }
       push(t1, 0.0, (unsigned)K);
       ++K;
@@ -161,7 +174,7 @@ struct CrbdLR {
                              uint32_t t, unsigned long long seed, double rho, NodeOut& out) {
     const uint4 B = side_block(seed, id, n, t, kTagNode);
     const double u0 = hq(B.x, B.y), u1 = hq(B.z, B.w);
-    const double d = -log(u0) * ow.inv_tot;   // Exp(lambda + mu)
+    const double d = -log_u(u0) * ow.inv_tot;   // Exp(lambda + mu)
     if (d > s) return u1 < rho ? NODE_DETECTED : NODE_LEAF;
     if (!(u1 < ow.pb)) return NODE_LEAF;                       // death
     const uint4 Cb = side_block(seed, id, n, t, kTagChild);
@@ -187,10 +200,10 @@ struct CrbdLR {
 #define SMC_CLADS2_FN __device__ __forceinline__
 #endif
 SMC_CLADS2_FN double clads2_bm(double u1, double u2) {            // N(0,1) (R-3, cos branch)
-  return 0.0 + 1.0 * (sqrt(-2.0 * log(u1)) * cospi(2.0 * u2));
+  return 0.0 + 1.0 * (sqrt(-2.0 * log_u(u1)) * cospi(2.0 * u2));
 }
 SMC_CLADS2_FN double2 clads2_bm_pair(double u1, double u2) {      // Box-Muller pair (R-18)
-  const double rad = sqrt(-2.0 * log(u1));
+  const double rad = sqrt(-2.0 * log_u(u1));
   double sn, cs;
   sincospi(2.0 * u2, &sn, &cs);
   return make_double2(rad * cs, rad * sn);
@@ -296,7 +309,7 @@ struct Clads2LR {
       }
       double dt = 0.0;
       if (!split) {
-        dt = -log(u[0]) / s.lam;
+        dt = -log_u(u[0]) / s.lam;
         if (t - dt <= tc) {
           r.consume(1, u);
           lw = lw + (-s.eps * s.lam * (t - tc));
@@ -329,7 +342,7 @@ struct Clads2LR {
 #else
       r.peek6(u);
       if (!split) {
-        const double dt = -log(u[0]) / s.lam;
+        const double dt = -log_u(u[0]) / s.lam;
         if (t - dt <= tc) {
           r.consume(1, u);
           lw = lw + (-s.eps * s.lam * (t - tc));
@@ -378,7 +391,7 @@ struct Clads2LR {
       // their Philox blocks and the two Box-Muller chains computed side by side
       double u[6];
       r.peek6(u);
-      const double dt = -log(u[0]) / s.lam;
+      const double dt = -log_u(u[0]) / s.lam;
       if (t - dt <= tc) {
         r.consume(1, u);
         lw = lw + (-s.eps * s.lam * (t - tc));
@@ -432,7 +445,7 @@ struct Clads2LR {
     // taken as -log(u0) > s lam (1 + eps) (no division; the same decision up
     // to rounding, like the CUDA/glibc ulp differences), d itself only for a birth
     const double rate = lam * ow.opeps;
-    const double nl = -log(u0);
+    const double nl = -log_u(u0);
     if (nl > s * rate) return u1 < rho ? NODE_DETECTED : NODE_LEAF;
     if (!(u1 < ow.pb)) return NODE_LEAF;
 #if !SMC_CLADS2_SPEC_Z

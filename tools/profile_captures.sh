@@ -20,9 +20,9 @@ cap crbd_lrw_e3 propagate_lrw_kernel 3 crbd
 cap crbd_lrw_e60 propagate_lrw_kernel 60 crbd
 cap clads2_lrw_e100 propagate_lrw_kernel 100 clads2
 cap crbd_fused_e100 resample_fused_kernel 100 crbd
-cap seir_prop_e100 "propagate_kernel<smc::Seir>" 100 seir
-cap fig3_prop_e10 "propagate_kernel<smc::Fig3>" 10 fig3
-cap stackf_prop_e3 "propagate_kernel<smc::Stackf>" 3 stackf
+cap seir_prop_e100 "propagate_kernel" 100 seir
+cap fig3_prop_e10 "propagate_kernel" 10 fig3
+cap stackf_prop_e3 "propagate_kernel" 3 stackf
 cap stackf_fused_e3 resample_fused_kernel 3 stackf
 cap c4_anc_gather_2p26 anc_gather_kernel 1 resample --n 67108864
 ls -la $O
