@@ -328,7 +328,8 @@ int smc_plan_ranges(const uint64_t* w_lohi, int32_t world, uint64_t n_per, uint6
  * denominator of the "alu"-bound propagation kernels): launches a
  * divergence-free microkernel on the current device in which every lane of a
  * full-occupancy grid draws draws_per_thread Exp(rate) variates from its own
- * Philox4x32-10 stream (hq conversion, fp64 -log(u)/rate; R-1..R-3)
+ * Philox4x32-10 stream (hq conversion, the kernels' table-driven fp64 log of a
+ * uniform times a precomputed 1/rate; R-1..R-3, §7)
  * and writes their sum.  *draws_per_s = uniforms consumed per second, best of
  * three timed launches (CUDA events).  SMC_EINVAL for a NULL output or 0
  * draws; SMC_ECUDA without a device.  Allocates and frees its own buffer. */

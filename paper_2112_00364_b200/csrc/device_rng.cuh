@@ -87,6 +87,34 @@ __device__ __forceinline__ double log_u(double u) {
 #endif
 }
 
+// e^x by a 128-entry table of 2^(j/128) and a degree-5 expm1 (Tang's method;
+// tools/gen_expt_table.py: worst 0.99 ulp against 60-digit exponentials), for
+// the ClaDS2 rate factors e^{sigma z}; |x| > 700 (overflow / underflow
+// territory) falls back to exp().  ~10 instead of ~17 fp64 operations.
+#ifndef SMC_FAST_EXP
+#define SMC_FAST_EXP 0      // measured slower for ClaDS2 (160.7 -> 165.2 ms/sweep): off
+#endif
+#include "expt_table.cuh"
+__device__ __noinline__ double exp_far(double x) { return exp(x); }   // rare: one out-of-line copy
+__device__ __forceinline__ double exp_t(double x) {
+#if SMC_FAST_EXP
+  if (!(fabs(x) <= 700.0)) return exp_far(x);
+  const double kd = rint(x * SMC_EXPT_INV);
+  const int k = (int)kd;
+  double r = fma(-kd, SMC_EXPT_C_HI, x);
+  r = fma(-kd, SMC_EXPT_C_LO, r);
+  double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  p = fma(r, p, 1.0 / 6.0);
+  p = fma(r, p, 0.5);
+  p = fma(r * r, p, r);                             // expm1(r)
+  const double tj = __ldg(&c_expt_tab[k & 127]);
+  const double scale = __hiloint2double(((k >> 7) + 1023) << 20, 0);
+  return fma(tj, p, tj) * scale;
+#else
+  return exp(x);
+#endif
+}
+
 // 53-bit integer of the hq conversion and the double u = z 2^-53 + 2^-54.
 __device__ __forceinline__ unsigned long long hq_bits(uint32_t x, uint32_t y) {
   return (unsigned long long)x ^ ((unsigned long long)y << 21);

@@ -209,7 +209,7 @@ SMC_CLADS2_FN double2 clads2_bm_pair(double u1, double u2) {      // Box-Muller 
   return make_double2(rad * cs, rad * sn);
 }
 SMC_CLADS2_FN double clads2_rate(double alpha, double lam, double sigma, double z) {
-  return alpha * lam * exp(sigma * z);
+  return alpha * lam * exp_t(sigma * z);
 }
 
 struct Clads2LR {
