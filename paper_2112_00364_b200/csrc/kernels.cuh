@@ -1251,6 +1251,9 @@ __global__ void __launch_bounds__(kThreads) max_kernel(const double* lw, unsigne
 #ifndef SMC_FUSED_GALLOP
 #define SMC_FUSED_GALLOP 0
 #endif
+#ifndef SMC_FUSED_SCAN
+#define SMC_FUSED_SCAN 1      // slot -> source by a warp-local mark + max-scan (else binary search)
+#endif
 constexpr int kFT = SMC_FUSED_THREADS;   // threads per fused CTA
 #ifndef SMC_FUSED_MINB
 #define SMC_FUSED_MINB 2                 // resident CTAs per SM (register cap 64)
@@ -1488,11 +1491,54 @@ __global__ void __launch_bounds__(kFT, SMC_FUSED_MINB) resample_fused_kernel(Res
 #if SMC_FUSED_GALLOP
     const unsigned wspan = wB - wA;
 #endif
+#if SMC_FUSED_SCAN
+    // Slot -> source map without searches when the warp's slots fit the
+    // shared memory its particles' quantised weights occupied (dead after 2a:
+    // 8 B per particle = 2 slots): each particle with offspring marks the
+    // first slot of its run, an inclusive max-scan over the warp's slots
+    // carries the mark to every slot of the run (no barrier: warp-local).
+    const unsigned span = wB - wA;
+    const bool use_map = span <= 2u * (unsigned)wn;
+    // (volatile: 32-bit accesses only — the region held 64-bit weights, and
+    // ptxas must not pair neighbouring entries into 64-bit loads)
+    volatile unsigned* buf = reinterpret_cast<volatile unsigned*>(s_q + wk0);
+    if (use_map) {
+      for (unsigned i = lane; i < span; i += 32) buf[i] = 0u;
+      __syncwarp();
+      const int k0 = wk0 + lane * ipt;
+      unsigned Op = k0 ? s_O[k0 - 1] : s_O[blk];
+      for (int r = 0; r < ipt; ++r) {
+        const unsigned Ok = s_O[k0 + r];
+        if (Ok > Op) buf[Op - wA] = (unsigned)(k0 + r - wk0) + 1u;
+        Op = Ok;
+      }
+      __syncwarp();
+      const unsigned per = (span + 31u) / 32u;
+      const unsigned lo = min(span, lane * per), hi = min(span, lo + per);
+      unsigned mx = 0;
+      for (unsigned i = lo; i < hi; ++i) { mx = max(mx, buf[i]); buf[i] = mx; }
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, mx, d);
+        if (lane >= d) mx = max(mx, t);
+      }
+      unsigned ex = __shfl_up_sync(0xffffffffu, mx, 1);
+      if (lane == 0) ex = 0u;
+      for (unsigned i = lo; i < hi; ++i) buf[i] = max(buf[i], ex);
+      __syncwarp();
+    }
+#endif
     for (unsigned j0 = wA + lane; j0 < wB; j0 += 32 * U) {
       int src[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const unsigned j = j0 + 32 * u;
+#if SMC_FUSED_SCAN
+        if (use_map) {
+          src[u] = j < wB ? wk0 + (int)buf[j - wA] - 1 : wk0;
+          continue;
+        }
+#endif
         int lo = wk0, hi = wk0 + wn - 1;                // first particle with O_k > j
 #if SMC_FUSED_GALLOP
         // start at the proportional guess and gallop to a bracket (sources

@@ -39,6 +39,9 @@ namespace smc {
 #ifndef SMC_LR_OPT
 #define SMC_LR_OPT 1
 #endif
+#ifndef SMC_CRBD_SPEC_CHILD
+#define SMC_CRBD_SPEC_CHILD 0   // CRBD nodes: the daughters' id block before the event test
+#endif
 #ifndef SMC_CRBD_RECIP
 #define SMC_CRBD_RECIP 1        // CRBD branch walk: -log(u) * (1/lambda) instead of a division
 #endif
@@ -173,11 +176,16 @@ struct CrbdLR {
   __device__ static int node(double s, double, unsigned long long id, const Owner& ow, uint32_t n,
                              uint32_t t, unsigned long long seed, double rho, NodeOut& out) {
     const uint4 B = side_block(seed, id, n, t, kTagNode);
+#if SMC_CRBD_SPEC_CHILD
+    const uint4 Cb = side_block(seed, id, n, t, kTagChild);    // speculative: independent of B
+#endif
     const double u0 = hq(B.x, B.y), u1 = hq(B.z, B.w);
     const double d = -log_u(u0) * ow.inv_tot;   // Exp(lambda + mu)
     if (d > s) return u1 < rho ? NODE_DETECTED : NODE_LEAF;
     if (!(u1 < ow.pb)) return NODE_LEAF;                       // death
+#if !SMC_CRBD_SPEC_CHILD
     const uint4 Cb = side_block(seed, id, n, t, kTagChild);
+#endif
     out.s2 = s - d;
     out.la = out.lb = 0.0;
     out.ida = ((unsigned long long)Cb.y << 32) | Cb.x;
