@@ -66,8 +66,7 @@ __device__ __forceinline__ uint4 philox_site(uint4 c, uint32_t k0, uint32_t k1) 
 #define SMC_FAST_LOGU 1
 #endif
 #include "logu_table.cuh"
-__device__ __forceinline__ double log_u(double u) {
-#if SMC_FAST_LOGU
+__device__ __forceinline__ double log_table(double u) {
   const long long ix = __double_as_longlong(u);
   const long long tmp = ix - 0x3fe6a09e667f3bcdLL;
   const int i = (int)((tmp >> 45) & 127);
@@ -82,8 +81,27 @@ __device__ __forceinline__ double log_u(double u) {
   p = fma(r, p, -0.5);
   const double l1 = fma(r * r, p, r);
   return fma(kd, SMC_LOGU_LN2_HI, t.y) + fma(kd, SMC_LOGU_LN2_LO, l1);
+}
+__device__ __forceinline__ double log_u(double u) {
+#if SMC_FAST_LOGU
+  return log_table(u);
 #else
   return log(u);
+#endif
+}
+// The same for any x: the table path serves positive normal finite x (the
+// reduction holds for any exponent); 0, subnormals, inf and NaN take the
+// library log out of line (one copy).  Used for log(lambda) weight terms.
+__device__ __noinline__ double log_far(double x) { return log(x); }
+#ifndef SMC_FAST_LOGPOS
+#define SMC_FAST_LOGPOS 1
+#endif
+__device__ __forceinline__ double log_pos(double x) {
+#if SMC_FAST_LOGU && SMC_FAST_LOGPOS
+  if (!(x >= 0x1p-1022 && x <= 0x1.fffffffffffffp+1023)) return log_far(x);
+  return log_table(x);
+#else
+  return log(x);
 #endif
 }
 

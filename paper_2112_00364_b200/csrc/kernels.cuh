@@ -1252,7 +1252,7 @@ __global__ void __launch_bounds__(kThreads) max_kernel(const double* lw, unsigne
 #define SMC_FUSED_GALLOP 0
 #endif
 #ifndef SMC_FUSED_SCAN
-#define SMC_FUSED_SCAN 1      // slot -> source by a warp-local mark + max-scan (else binary search)
+#define SMC_FUSED_SCAN 0      // warp-local mark + max-scan slot map: measured no faster (CRBD resampling 7.25 -> 7.35 ms/sweep), off
 #endif
 constexpr int kFT = SMC_FUSED_THREADS;   // threads per fused CTA
 #ifndef SMC_FUSED_MINB

@@ -134,7 +134,7 @@ struct CrbdLR {
     const double tp = __ldg(b), tc = __ldg(b + 1);
     const bool internal = __ldg(b + 2) != 0.0;
     lw = lw + (-s.mu * (tp - tc));
-    lw = lw + (internal ? log(s.lambda) : log(rho));
+    lw = lw + (internal ? log_pos(s.lambda) : log(rho));
     const double tot = s.lambda + s.mu;   // before any push: phase-2 lanes read them
     ow.inv_tot = 1.0 / tot;
     ow.pb = s.lambda / tot;
@@ -322,7 +322,7 @@ struct Clads2LR {
           r.consume(1, u);
           lw = lw + (-s.eps * s.lam * (t - tc));
           if (!internal) break;
-          lw = lw + log(s.lam);
+          lw = lw + log_pos(s.lam);
           split = true;
           continue;
         }
@@ -355,7 +355,7 @@ struct Clads2LR {
           r.consume(1, u);
           lw = lw + (-s.eps * s.lam * (t - tc));
           if (!internal) break;
-          lw = lw + log(s.lam);
+          lw = lw + log_pos(s.lam);
           split = true;
           continue;
         }
@@ -418,7 +418,7 @@ struct Clads2LR {
       if (Clads2::bad_rate(s.lam)) { killed = true; break; }
     }
     if (!killed && internal) {
-      lw = lw + log(s.lam);
+      lw = lw + log_pos(s.lam);
       double u[6];                           // z_l, z_r: the four uniforms of two d_normal calls
       r.peek6(u);
       r.consume(4, u);

@@ -116,7 +116,7 @@ struct Crbd {
     const double tp = __ldg(b), tc = __ldg(b + 1);
     const bool internal = __ldg(b + 2) != 0.0;
     lw = lw + (-s.mu * (tp - tc));
-    lw = lw + (internal ? log(s.lambda) : log(rho));
+    lw = lw + (internal ? log_pos(s.lambda) : log(rho));
     double t = tp;
     for (;;) {
       t = t - d_exp(r, s.lambda);
@@ -168,13 +168,13 @@ struct CrbdAE : Crbd {
     const double tp = __ldg(b), tc = __ldg(b + 1);
     const bool internal = __ldg(b + 2) != 0.0;
     lw = lw + (-s.mu * (tp - tc));
-    lw = lw + (internal ? log(s.lambda) : log(rho));
+    lw = lw + (internal ? log_pos(s.lambda) : log(rho));
     double t = tp;
     for (;;) {
       t = t - d_exp(r, s.lambda);
       if (t <= tc) break;
       lw = lw + kLn2;
-      lw = lw + log(crbd_no_sampled_descendant(t, s.lambda, s.mu, rho));
+      lw = lw + log_pos(crbd_no_sampled_descendant(t, s.lambda, s.mu, rho));
     }
     s.branch = s.branch + 1;
     s.pc = (s.branch == C.n) ? kStop : 1;
@@ -319,7 +319,7 @@ struct Clads2 {
       if (bad_rate(s.lam)) { killed = true; break; }
     }
     if (!killed && internal) {
-      lw = lw + log(s.lam);
+      lw = lw + log_pos(s.lam);
       const double zl = d_normal(r, 0.0, 1.0);
       const double zr = d_normal(r, 0.0, 1.0);
       const double rl = daughter(s, s.lam, zl), rr = daughter(s, s.lam, zr);
