@@ -94,7 +94,7 @@ __device__ __forceinline__ double log_u(double u) {
 // library log out of line (one copy).  Used for log(lambda) weight terms.
 __device__ __noinline__ double log_far(double x) { return log(x); }
 #ifndef SMC_FAST_LOGPOS
-#define SMC_FAST_LOGPOS 1
+#define SMC_FAST_LOGPOS 0      // measured neutral (CRBD 48.5 vs 48.6, ClaDS2 156.5 vs 157.0 ms): library log for weight terms
 #endif
 __device__ __forceinline__ double log_pos(double x) {
 #if SMC_FAST_LOGU && SMC_FAST_LOGPOS
@@ -130,6 +130,37 @@ __device__ __forceinline__ double exp_t(double x) {
   return fma(tj, p, tj) * scale;
 #else
   return exp(x);
+#endif
+}
+
+// cos and sin of 2 pi t for a uniform t in (0, 1) (the Box-Muller angle):
+// j = rint(256 t), r = t - j/256 exactly, x = 2 pi r, |x| <= pi/256;
+// cos(2 pi t) = C_j cos x - S_j sin x (sin likewise) with a 256-entry table of
+// (C_j, S_j) and Taylor polynomials to x^6 / x^7 (tools/gen_trig_table.py:
+// absolute error <= 1.6e-16, below that of cos(fl(2 pi u)) itself).
+#ifndef SMC_FAST_TRIG
+#define SMC_FAST_TRIG 1
+#endif
+#include "trig_table.cuh"
+__device__ __forceinline__ double2 sincos2pi_u(double t) {      // (sin, cos)
+  const double jd = rint(t * 256.0);
+  const double r = t - jd * (1.0 / 256.0);
+  const double x = r * SMC_TRIG_TWO_PI;
+  const double x2 = x * x;
+  double cm = fma(x2, -1.0 / 720.0, 1.0 / 24.0);
+  cm = fma(x2, cm, -0.5);
+  cm = x2 * cm;                                     // cos x - 1
+  double sp = fma(x2, -1.0 / 5040.0, 1.0 / 120.0);
+  sp = fma(x2, sp, -1.0 / 6.0);
+  const double sx = fma(x * x2, sp, x);             // sin x
+  const double2 cs = __ldg(&c_trig_tab[(int)jd & 255]);
+  return make_double2(fma(cs.y, cm, fma(cs.x, sx, cs.y)), fma(cs.x, cm, fma(-cs.y, sx, cs.x)));
+}
+__device__ __forceinline__ double cos2pi_u(double t) {
+#if SMC_FAST_TRIG
+  return sincos2pi_u(t).y;
+#else
+  return cospi(2.0 * t);
 #endif
 }
 
@@ -218,7 +249,7 @@ __device__ __forceinline__ double d_normal(Rng& r, double mu, double sigma) {
   const double u1 = r.uniform();
   const double u2 = r.uniform();
   const double rad = sqrt(-2.0 * log_u(u1));
-  const double c = cospi(2.0 * u2);          // cos(2 pi u2) without a 2 pi range reduction
+  const double c = cos2pi_u(u2);          // cos(2 pi u2) without a 2 pi range reduction
   return mu + sigma * (rad * c);
 }
 __device__ __noinline__ double d_gamma_mt(Rng& r, double k, double theta) {   // k > 1, Marsaglia-Tsang

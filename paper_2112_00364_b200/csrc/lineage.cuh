@@ -208,13 +208,18 @@ struct CrbdLR {
 #define SMC_CLADS2_FN __device__ __forceinline__
 #endif
 SMC_CLADS2_FN double clads2_bm(double u1, double u2) {            // N(0,1) (R-3, cos branch)
-  return 0.0 + 1.0 * (sqrt(-2.0 * log_u(u1)) * cospi(2.0 * u2));
+  return 0.0 + 1.0 * (sqrt(-2.0 * log_u(u1)) * cos2pi_u(u2));
 }
 SMC_CLADS2_FN double2 clads2_bm_pair(double u1, double u2) {      // Box-Muller pair (R-18)
   const double rad = sqrt(-2.0 * log_u(u1));
+#if SMC_FAST_TRIG
+  const double2 sc = sincos2pi_u(u2);
+  return make_double2(rad * sc.y, rad * sc.x);
+#else
   double sn, cs;
   sincospi(2.0 * u2, &sn, &cs);
   return make_double2(rad * cs, rad * sn);
+#endif
 }
 SMC_CLADS2_FN double clads2_rate(double alpha, double lam, double sigma, double z) {
   return alpha * lam * exp_t(sigma * z);
