@@ -116,7 +116,14 @@ __device__ __forceinline__ double log_pos(double x) {
 __device__ __noinline__ double exp_far(double x) { return exp(x); }   // rare: one out-of-line copy
 __device__ __forceinline__ double exp_t(double x) {
 #if SMC_FAST_EXP
+#if SMC_FAST_EXP == 2
+  // clamped instead of a far path: e^{+-700} stands in for inf / 0 (a rate
+  // factor that large breaks the rate guard either way; one that small makes
+  // every event time exceed the branch, as a zero rate does)
+  x = fmin(fmax(x, -700.0), 700.0);
+#else
   if (!(fabs(x) <= 700.0)) return exp_far(x);
+#endif
   const double kd = rint(x * SMC_EXPT_INV);
   const int k = (int)kd;
   double r = fma(-kd, SMC_EXPT_C_HI, x);
