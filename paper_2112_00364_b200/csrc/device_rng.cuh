@@ -108,10 +108,11 @@ __device__ __forceinline__ double log_pos(double x) {
 // e^x by a 128-entry table of 2^(j/128) and a degree-5 expm1 (Tang's method;
 // tools/gen_expt_table.py: worst 0.99 ulp against 60-digit exponentials), for
 // the ClaDS2 rate factors e^{sigma z}; |x| > 700 (overflow / underflow
-// territory) falls back to exp().  ~10 instead of ~17 fp64 operations.
+// territory) is clamped (or, SMC_FAST_EXP=1, goes to exp()).  ~10 instead of
+// ~17 fp64 operations.
 #ifndef SMC_FAST_EXP
-#define SMC_FAST_EXP 0      // measured slower for ClaDS2 (160.7 -> 165.2 ms/sweep): off
-#endif
+#define SMC_FAST_EXP 2      // 2: clamped to |x| <= 700 (ClaDS2 156.6 -> 153.6 ms/sweep); 1: out-of-line
+#endif                      // library exp beyond 700 (measured slower, 160.7 -> 165.2); 0: library exp
 #include "expt_table.cuh"
 __device__ __noinline__ double exp_far(double x) { return exp(x); }   // rare: one out-of-line copy
 __device__ __forceinline__ double exp_t(double x) {
