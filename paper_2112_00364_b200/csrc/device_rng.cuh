@@ -307,17 +307,45 @@ struct LogFact {
 // Binomial: inversion (BINV) for n p < 10; BTRS (Hormann 1993) otherwise.
 // The BTRS normaliser h = lgamma(m+1) + lgamma(n-m+1) is only needed when
 // the squeeze fails, so it is computed lazily (same value, fewer lgammas).
+// SMC_FAST_BINOM: the same formulas with the table-driven log / exp of §7.8
+// (log1p(y) = log u + (y - (u - 1)) / u for u = fl(1 + y), the tiny
+// correction divided by a float reciprocal), 1/x from a table in the
+// inversion loop, and the BTRS acceptance log by the table: ulp-level
+// differences, as the CUDA/glibc transcendentals have.
+#ifndef SMC_FAST_BINOM
+#define SMC_FAST_BINOM 1
+#endif
+struct RcpTab { double v[128]; };
+constexpr RcpTab make_rcp_tab() {
+  RcpTab t{};
+  for (int i = 1; i < 128; ++i) t.v[i] = 1.0 / (double)i;
+  return t;
+}
+__device__ const RcpTab c_rcp_tab = make_rcp_tab();
+__device__ __forceinline__ double log1p_neg(double y) {            // y in [-1/2, 0]
+  const double u = 1.0 + y;
+  const double c = y - (u - 1.0);                                   // exact (Sterbenz)
+  return log_table(u) + c * (double)__frcp_rn((float)u);
+}
 __device__ __noinline__ long long d_binomial_inv(Rng& r, long long n, double p) {
   const double q = 1.0 - p;
   const double sr = p / q;
   const double a = (double)(n + 1) * sr;
+#if SMC_FAST_BINOM
+  double pr = exp_t((double)n * log1p_neg(-p));
+#else
   double pr = exp((double)n * log1p(-p));
+#endif
   double u = r.uniform_compact();
   long long x = 0;
   while (x < n && u > pr) {
     u = u - pr;
     x = x + 1;
+#if SMC_FAST_BINOM
+    pr = pr * ((x < 128 ? a * c_rcp_tab.v[x] : a / (double)x) - sr);
+#else
     pr = pr * (a / (double)x - sr);
+#endif
   }
   return x;
 }
@@ -345,7 +373,11 @@ __device__ __noinline__ long long d_binomial_btrs(Rng& r, long long n, double p,
       h = lf(m + 1.0) + lf(nd - m + 1.0);
       have_h = true;
     }
+#if SMC_FAST_BINOM
+    const double lv = log_table(V * alpha / (a / (us * us) + b));
+#else
     const double lv = log(V * alpha / (a / (us * us) + b));
+#endif
     const double rhs = h - lf(kd + 1.0) - lf(nd - kd + 1.0) + (kd - m) * lpq;
     if (lv <= rhs) return (long long)kd;
   }
