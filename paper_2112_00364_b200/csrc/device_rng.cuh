@@ -369,7 +369,11 @@ __device__ __noinline__ long long d_binomial_btrs(Rng& r, long long n, double p,
     if (us >= 0.07 && V <= vr) return (long long)kd;
     if (!have_h) {
       alpha = (2.83 + 5.1 / b) * spq;
+#if SMC_FAST_BINOM
+      lpq = log_table(p / q);
+#else
       lpq = log(p / q);
+#endif
       h = lf(m + 1.0) + lf(nd - m + 1.0);
       have_h = true;
     }

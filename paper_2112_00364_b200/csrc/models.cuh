@@ -397,8 +397,13 @@ struct Seir {
     }
     const LogFact lf{C.logfact, C.n_logfact};
     const double nh = (double)nh_i;                      // DAY
+#if SMC_FAST_BINOM
+    const double ph = 1.0 - exp_t(-(double)s.im / nh);    // (table exp, §7.8)
+    const double pm = 1.0 - exp_t(-(double)s.ih / nh);
+#else
     const double ph = 1.0 - exp(-(double)s.im / nh);
     const double pm = 1.0 - exp(-(double)s.ih / nh);
+#endif
     const long long tau_h = d_binomial(r, s.sh, ph, lf);
     const long long de_h = d_binomial(r, tau_h, s.lam_h, lf);
     const long long di_h = d_binomial(r, s.eh, s.del_h, lf);
