@@ -177,7 +177,8 @@ __device__ __forceinline__ unsigned long long hq_bits(uint32_t x, uint32_t y) {
   return (unsigned long long)x ^ ((unsigned long long)y << 21);
 }
 __device__ __forceinline__ double hq(uint32_t x, uint32_t y) {
-  return __dadd_rn(__dmul_rn(__ull2double_rn(hq_bits(x, y)), 0x1p-53), 0x1p-54);
+  // z 2^-53 is exact (z < 2^53), so one fma rounds exactly where the add did
+  return __fma_rn(__ull2double_rn(hq_bits(x, y)), 0x1p-53, 0x1p-54);
 }
 
 // Per-particle uniform stream for one epoch (registers only; SoA state holds
