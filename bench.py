@@ -653,7 +653,7 @@ def sweep_line(args, name, wl, smc, torch, world, rank, pk, pk_kind, draw_peak, 
     if rank == 0 and with_cpu and world == 1:
         cpu = oracle_sweep_rate(wl, budget_s=args.cpu_budget)
     spec = None
-    if lin:
+    if lin and rank == 0:           # (reported by rank 0 only; no collectives inside)
         # Under R-18 the GPU's count depends on its visiting order (speculative
         # side-tree nodes evaluated before a detection elsewhere stops the tree,
         # and nodes a depth-first walk would have reached first but that were
