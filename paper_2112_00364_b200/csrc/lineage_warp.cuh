@@ -40,6 +40,9 @@ constexpr int kWMax = SMC_LRW_WMAX;              // lanes one owner may take in 
 #ifndef SMC_LRW_FASTMAP
 #define SMC_LRW_FASTMAP 1
 #endif
+#ifndef SMC_LRW_BALLOT_SCAN
+#define SMC_LRW_BALLOT_SCAN 1   // offsets of the per-owner task counts: bit-sliced ballots (1) or shuffles (0)
+#endif
 #ifndef SMC_LRW_BALLOTPUSH
 #define SMC_LRW_BALLOTPUSH 0      // ballot-ranked pushes instead of shared atomics: measured slower (CRBD 53.8 -> 57.0, ClaDS2 188 -> 196 ms)
 #endif
@@ -104,7 +107,7 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
   double* w_tlam = s_tlam[warp];
   // task records: the bottom kSm slots of each owner's segment live in shared
   // memory (small stacks never leave the SM), the rest in this warp's region
-  auto put = [&](unsigned long long slot, double s0, double lam0, unsigned long long id) {
+  auto put = [&](unsigned slot, double s0, double lam0, unsigned long long id) {
     const double2 v = make_double2(s0, __longlong_as_double((long long)id));
     if (kSm > 0 && slot < kWSegSlots && (int)(slot % kWSeg) < kSm) {
       const int k = (int)(slot / kWSeg) * kSm + (int)(slot % kWSeg);
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
     T_sid[slot] = v;
     if (M::kHasLam) T_lam[slot] = lam0;
   };
-  auto get = [&](unsigned long long slot, double2& v, double& lam0) {
+  auto get = [&](unsigned slot, double2& v, double& lam0) {
     if (kSm > 0 && slot < kWSegSlots && (int)(slot % kWSeg) < kSm) {
       const int k = (int)(slot / kWSeg) * kSm + (int)(slot % kWSeg);
       v = w_tsk[k];
@@ -126,12 +129,12 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
     if (M::kHasLam) lam0 = T_lam[slot];
   };
   // overflow slot for owner o (-1: the warp's stack is full -> task-cap error)
-  auto ovf_slot = [&](int o) -> long long {
+  auto ovf_slot = [&](int o) -> int {
     const int q = atomicAdd(w_ovtop, 1);
     if (q >= kWOvf) { s_taskcap = 1; return -1; }
-    const unsigned long long slot = kWSegSlots + (unsigned long long)q;
+    const int slot = (int)kWSegSlots + q;
     T_own[slot] = (unsigned short)o;
-    return (long long)slot;
+    return slot;
   };
 
   long long key = LLONG_MIN;
@@ -172,10 +175,10 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
         ++n_start;
         Rng r(seed, (uint32_t)(p.shard_base + i), epoch);
         auto push = [&](double s0, double lam0, unsigned kk) {
-          long long slot;
-          if (c < kWSeg) slot = (long long)lane * kWSeg + c++;
+          int slot;
+          if (c < kWSeg) slot = lane * kWSeg + c++;
           else slot = ovf_slot(lane);
-          if (slot >= 0) put((unsigned long long)slot, s0, lam0, root_id(kk));
+          if (slot >= 0) put((unsigned)slot, s0, lam0, root_id(kk));
         };
         if (!M::main_part(st, lw, r, C, w_own[lane], K, push)) dead = 3;   // rate guard
         roots += (unsigned)K;
@@ -202,6 +205,7 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
       // (independent, no shuffle chain); the owner of a lane is the last task
       // range starting at or below it: a bitmask of range starts (one
       // redux.sync) and one shared-memory read of (owner, its count) at that start
+#if SMC_LRW_BALLOT_SCAN
       int incl = 0, T = 0;
 #pragma unroll
       for (int b = 0; b < 6; ++b) {
@@ -210,23 +214,32 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
         T += __popc(bb) << b;
       }
       T = min(T, 32);
+#else
+      int incl = m;                                     // shuffle scan (fewer instructions, longer chain)
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(FULL, incl, d);
+        if (lane >= d) incl += t;
+      }
+      const int T = min(__shfl_sync(FULL, incl, 31), 32);
+#endif
       const int off = incl - m;
       const int me = max(0, min(m, 32 - off));
       if (me > 0) w_start[off] = (c << 5) | lane;
       const unsigned starts = __reduce_or_sync(FULL, me > 0 ? (1u << off) : 0u);
       __syncwarp();
       bool have = false;
-      unsigned long long slot = 0;
+      unsigned slot = 0;
       int ow = 0, s0 = 0;
       if (lane < T) {
         s0 = 31 - __clz(starts & le_mask);             // this lane's range start
         const int sv = w_start[s0];
         have = true;
         ow = sv & 31;
-        slot = (unsigned long long)ow * kWSeg + (unsigned long long)((sv >> 5) - 1 - (lane - s0));
+        slot = (unsigned)(ow * kWSeg + ((sv >> 5) - 1 - (lane - s0)));
       } else if (lane - T < ov) {
         have = true;
-        slot = kWSegSlots + (unsigned long long)(ov - 1 - (lane - T));
+        slot = (unsigned)kWSegSlots + (unsigned)(ov - 1 - (lane - T));
         ow = (int)T_own[slot];
       }
       c -= me;                                          // pops (the owner's base for pushes)
@@ -258,15 +271,15 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
       const int c_o = __shfl_sync(FULL, c, osrc);
       const int off_o = __shfl_sync(FULL, off, osrc);
       bool have = false;
-      unsigned long long slot = 0;
+      unsigned slot = 0;
       int ow = 0;
       if (lane < T) {
         have = true;
         ow = o;
-        slot = (unsigned long long)o * kWSeg + (unsigned long long)(c_o - 1 - (lane - off_o));
+        slot = (unsigned)(o * kWSeg + (c_o - 1 - (lane - off_o)));
       } else if (lane - T < ov) {
         have = true;
-        slot = kWSegSlots + (unsigned long long)(ov - 1 - (lane - T));
+        slot = (unsigned)kWSegSlots + (unsigned)(ov - 1 - (lane - T));
         ow = (int)T_own[slot];
       }
       c -= me;                                          // pops (the owner's base for pushes)
@@ -303,18 +316,18 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
       const unsigned gmask = __ballot_sync(FULL, segl && res == NODE_GUARD);
       if (segl && res == NODE_BIRTH) {
         const int b = base_ow + 2 * __popc(bmask & (le_mask >> 1) & (0xffffffffu << s0));
-        const long long s1 = b < kWSeg ? (long long)ow * kWSeg + b : ovf_slot(ow);
-        const long long s2 = b + 1 < kWSeg ? (long long)ow * kWSeg + b + 1 : ovf_slot(ow);
-        if (s1 >= 0) put((unsigned long long)s1, out.s2, out.lb, out.idb);
-        if (s2 >= 0) put((unsigned long long)s2, out.s2, out.la, out.ida);   // first daughter on top
+        const int s1 = b < kWSeg ? ow * kWSeg + b : ovf_slot(ow);
+        const int s2 = b + 1 < kWSeg ? ow * kWSeg + b + 1 : ovf_slot(ow);
+        if (s1 >= 0) put((unsigned)s1, out.s2, out.lb, out.idb);
+        if (s2 >= 0) put((unsigned)s2, out.s2, out.la, out.ida);   // first daughter on top
       } else if (run && !segl) {                        // a task from the overflow stack
         atomicAdd(&w_ovn[ow], 1);
         if (res == NODE_DETECTED || res == NODE_GUARD) {
           atomicCAS(&w_det[ow], 0, res == NODE_GUARD ? 3 : 1);
         } else if (res == NODE_BIRTH) {
-          const long long s1 = ovf_slot(ow), s2 = ovf_slot(ow);
-          if (s1 >= 0) put((unsigned long long)s1, out.s2, out.lb, out.idb);
-          if (s2 >= 0) put((unsigned long long)s2, out.s2, out.la, out.ida);
+          const int s1 = ovf_slot(ow), s2 = ovf_slot(ow);
+          if (s1 >= 0) put((unsigned)s1, out.s2, out.lb, out.idb);
+          if (s2 >= 0) put((unsigned)s2, out.s2, out.la, out.ida);
         }
       }
       __syncwarp();
@@ -348,10 +361,10 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
           atomicCAS(&w_det[ow], 0, res == NODE_GUARD ? 3 : 1);
         } else if (res == NODE_BIRTH) {
           const int b = base_ow + atomicAdd(&w_push[ow], 2);
-          const long long s1 = b < kWSeg ? (long long)ow * kWSeg + b : ovf_slot(ow);
-          const long long s2 = b + 1 < kWSeg ? (long long)ow * kWSeg + b + 1 : ovf_slot(ow);
-          if (s1 >= 0) put((unsigned long long)s1, out.s2, out.lb, out.idb);
-          if (s2 >= 0) put((unsigned long long)s2, out.s2, out.la, out.ida);   // first daughter on top
+          const int s1 = b < kWSeg ? ow * kWSeg + b : ovf_slot(ow);
+          const int s2 = b + 1 < kWSeg ? ow * kWSeg + b + 1 : ovf_slot(ow);
+          if (s1 >= 0) put((unsigned)s1, out.s2, out.lb, out.idb);
+          if (s2 >= 0) put((unsigned)s2, out.s2, out.la, out.ida);   // first daughter on top
         }
       }
       __syncwarp();
