@@ -41,7 +41,7 @@ constexpr int kWMax = SMC_LRW_WMAX;              // lanes one owner may take in 
 #define SMC_LRW_FASTMAP 1
 #endif
 #ifndef SMC_LRW_BALLOT_SCAN
-#define SMC_LRW_BALLOT_SCAN 1   // offsets of the per-owner task counts: bit-sliced ballots (1) or shuffles (0)
+#define SMC_LRW_BALLOT_SCAN 0   // offsets by bit-sliced ballots (1) or a shuffle scan (0: CRBD 48.1 -> 46.75 ms)
 #endif
 #ifndef SMC_LRW_BALLOTPUSH
 #define SMC_LRW_BALLOTPUSH 0      // ballot-ranked pushes instead of shared atomics: measured slower (CRBD 53.8 -> 57.0, ClaDS2 188 -> 196 ms)
