@@ -516,3 +516,14 @@ def test_gather_modes_vs_oracle(smc, monkeypatch, kind, data, params, N, mode):
             "ssm": lambda: inputs.ssm_series(50), "seir": inputs.seir_series,
             "stackf": inputs.stackf_series}.get(data, lambda: data)()
     run_pair(smc, kind, data, params, N, 21)
+
+
+# ------------------------------------------------ CTA cooperative kernel (R-18)
+@pytest.mark.parametrize("kind,params,seed", [(oracle.CRBD_LR, inputs.CRBD_PARAMS, 93),
+                                              (oracle.CLADS2_LR, inputs.CLADS2_PARAMS, 94)])
+def test_lineage_cta_kernel_vs_oracle(smc, monkeypatch, kind, params, seed):
+    """The CTA version of the cooperative side-tree kernel (propagate_lr_kernel,
+    selected at handle creation by SMC_LR_KERNEL=cta) against the oracle on tree90,
+    element by element per epoch — the warp kernel is the default and covered above."""
+    monkeypatch.setenv("SMC_LR_KERNEL", "cta")
+    run_pair(smc, kind, inputs.tree("tree90"), params, 3000, seed, per_epoch=True)
