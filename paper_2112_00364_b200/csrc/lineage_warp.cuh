@@ -40,6 +40,9 @@ constexpr int kWMax = SMC_LRW_WMAX;              // lanes one owner may take in 
 #ifndef SMC_LRW_FASTMAP
 #define SMC_LRW_FASTMAP 1
 #endif
+#ifndef SMC_LRW_OVN_UNIFORM
+#define SMC_LRW_OVN_UNIFORM 1   // overflow-pop counters read and cleared only in rounds that popped overflow tasks
+#endif
 #ifndef SMC_LRW_BALLOT_SCAN
 #define SMC_LRW_BALLOT_SCAN 0   // offsets by bit-sliced ballots (1) or a shuffle scan (0: CRBD 48.1 -> 46.75 ms)
 #endif
@@ -369,8 +372,17 @@ __global__ void __launch_bounds__(kWThreads, M::kLRWMinBlocks) propagate_lrw_ker
       }
       __syncwarp();
       // owner updates
+#if SMC_LRW_OVN_UNIFORM
+      int ovn = 0;
+      if (ov) {                                         // (warp-uniform) overflow tasks this round
+        ovn = w_ovn[lane];
+        w_ovn[lane] = 0;
+      }
+      const int dc = w_det[lane], pushed = w_push[lane];
+#else
       const int ovn = w_ovn[lane], dc = w_det[lane], pushed = w_push[lane];
       w_ovn[lane] = 0;
+#endif
       w_det[lane] = 0;
       w_push[lane] = 0;
       if (dead == 0) {
