@@ -41,7 +41,7 @@ constexpr int kWMax = SMC_LRW_WMAX;              // lanes one owner may take in 
 #define SMC_LRW_FASTMAP 1
 #endif
 #ifndef SMC_LRW_OVN_UNIFORM
-#define SMC_LRW_OVN_UNIFORM 1   // overflow-pop counters read and cleared only in rounds that popped overflow tasks
+#define SMC_LRW_OVN_UNIFORM 0   // overflow-pop counters only in rounds with overflow pops: measured slower (46.7 -> 47.3 ms), off
 #endif
 #ifndef SMC_LRW_BALLOT_SCAN
 #define SMC_LRW_BALLOT_SCAN 0   // offsets by bit-sliced ballots (1) or a shuffle scan (0: CRBD 48.1 -> 46.75 ms)
