@@ -52,7 +52,7 @@ namespace smc {
 #define SMC_CLADS2_LAZYPEEK 0   // Philox blocks only as far as used: measured slower (181.0 -> 187.0 ms; the look-ahead ILP wins)
 #endif
 #ifndef SMC_CLADS2_SPEC_Z
-#define SMC_CLADS2_SPEC_Z 1     // ClaDS2 nodes: daughters' noise block before the event test (measured -1.3%)
+#define SMC_CLADS2_SPEC_Z 0     // daughters' noise block before the event test: 1.3% faster in round 1, 0.7% slower on the final kernel (149.8 vs 150.8 ms)
 #endif
 constexpr int kLRThreads = SMC_LR_THREADS;     // threads per CTA = lanes per cooperative round
 constexpr int kOPT = SMC_LR_OPT;                 // particles (owners) per thread
